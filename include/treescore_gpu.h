@@ -1,0 +1,143 @@
+/*
+ * treescore_gpu.h -- C ABI of the B200 tree-ensemble scoring engine.
+ *
+ * Drop-in boundary for the reference package `treescore` (pure Python; its
+ * only native crossing is the ctypes-loaded CodeGen unit, codegen.py:150-167).
+ * Every entry point is plain C: pointers, sizes and status codes, no torch
+ * types.  Errors return a nonzero ts_status and set a thread-local message
+ * (ts_last_error); no entry point aborts the process.
+ *
+ *   reference interface                        replaced by
+ *   ----------------------------------------   ------------------------------
+ *   VPredicatedEvaluator.__init__               ts_pack
+ *     (evaluators.py:490-512; expand_to_complete model.py:315-349)
+ *   VPredicatedEvaluator._predict_into          ts_score  (device buffers,
+ *     (evaluators.py:520-546; batch kernel        stream-ordered)
+ *      evaluators.py:90-99)
+ *   GeneratedUnit score_batch(const float *x,   ts_score_host (host buffers,
+ *     int64_t n, int64_t f, double *out)          same argument meaning)
+ *     (codegen.py:115-121, :173-179)
+ *   GeneratedUnit score_ensemble(const float*)  ts_score_host with n = 1
+ *     (codegen.py:108-113)
+ *   leaf_index_predicated / batch_kernel        ts_score with ord_out != NULL
+ *     ordinals (evaluators.py:122-134, :90-99)
+ *   Evaluator.stored_node_count                 ts_model_info.table_entries
+ *     (evaluators.py:197-200, :548-550)
+ *   DepthLimitError (model.py:70-71, :324-327)  TS_ERR_DEPTH
+ *   ValueError dataset shape (evaluators.py:212-220)  TS_ERR_SHAPE
+ *   Dataset non-finite ValueError (data.py:50-51)     TS_ERR_NONFINITE
+ *
+ * Semantics (identical to the reference predicated kinds): a node sends x
+ * right iff x[fid] >= threshold (ties go right); dummy padding nodes
+ * (fid 0, theta +inf) always go left for finite x; the per-tree leaf ordinal
+ * is the predicated ordinal of the tree's complete expansion to its own
+ * depth; scores are acc = +0.0; acc = acc + weight * (double)leaf in tree
+ * order, f64, multiply then add (no FMA) -- bit-identical to the reference.
+ */
+#ifndef TREESCORE_GPU_H
+#define TREESCORE_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    TS_OK = 0,
+    TS_ERR_INVALID = 1,      /* malformed model description or argument   */
+    TS_ERR_DEPTH = 2,        /* tree deeper than TS_MAX_DEPTH              */
+    TS_ERR_SHAPE = 3,        /* f != model num_features, bad ld / sizes    */
+    TS_ERR_NONFINITE = 4,    /* instance matrix holds NaN or +-inf         */
+    TS_ERR_CUDA = 5,         /* CUDA runtime failure (message has details) */
+    TS_ERR_NOMEM = 6,
+    TS_ERR_UNSUPPORTED = 7
+} ts_status;
+
+#define TS_MAX_DEPTH 16
+
+/* Flat logical model (the text model format's shape, SPEC "External
+ * Interfaces" / model.py:356-387): trees in evaluation order; the nodes of
+ * tree t are [tree_node_offset[t], tree_node_offset[t+1]) with tree-local
+ * ids, id 0 the root.  node_fid[i] == -1 marks a leaf.  node_value is the
+ * fp32 threshold (internal) or fp32 leaf value (leaf).  node_left/right are
+ * tree-local child ids (ignored for leaves). */
+typedef struct {
+    int32_t num_features;
+    int32_t num_trees;
+    const int64_t *tree_node_offset;   /* [num_trees + 1] */
+    const double *tree_weight;         /* [num_trees], finite */
+    const int32_t *node_fid;
+    const float *node_value;
+    const int32_t *node_left;
+    const int32_t *node_right;
+} ts_model_desc;
+
+typedef struct ts_model ts_model;
+
+typedef struct {
+    int32_t num_features;
+    int32_t num_trees;
+    int32_t max_depth;
+    int32_t num_segments;          /* kernel launches per ts_score call     */
+    int64_t sum_depth;             /* sum over trees of d_t (visits/instance) */
+    int64_t table_entries;         /* sum 2^(d_t+1)-1: ref stored_node_count */
+    int64_t device_bytes;          /* packed tables resident on the device  */
+    int32_t complete_trees;        /* trees packed in the implicit heap form */
+    int32_t compact_trees;         /* trees packed in the child-index form   */
+    int32_t device;
+    int32_t unit_weights;          /* all weights == 1.0 */
+} ts_model_info;
+
+/* Validate, pack and upload a model to `device`.  The description is only
+ * read during the call.  Returns TS_ERR_INVALID / TS_ERR_DEPTH on bad
+ * models with a message naming the tree. */
+int ts_pack(const ts_model_desc *desc, int device, ts_model **out);
+
+int ts_model_get_info(const ts_model *model, ts_model_info *info);
+
+/* Score n instances already resident on the model's device.
+ *   x        fp32 [n, f] row-major, row stride ld >= f (elements)
+ *   out      f64 [n]
+ *   ord_out  nullable; uint16 [num_trees, ld_ord] predicated leaf ordinals
+ *            (tree-major so that rows are contiguous), ld_ord >= n
+ *   status   nullable; int32 device word, OR-ed with 1 if any x is NaN/inf
+ *   stream   cudaStream_t (NULL = legacy default stream)
+ * Stream-ordered; allocates nothing; returns after enqueueing. */
+int ts_score(const ts_model *model, const float *x, int64_t n, int64_t f, int64_t ld,
+             double *out, uint16_t *ord_out, int64_t ld_ord, int32_t *status,
+             void *stream);
+
+/* Host-buffer scoring: same argument meaning as the reference's generated
+ * score_batch(x, n, f, out).  Copies x to the device in chunks on two
+ * streams (H2D of chunk i+1 overlaps scoring of chunk i), copies the scores
+ * back, synchronises.  Pinned host memory gives full PCIe bandwidth; any
+ * host memory is accepted.  Returns TS_ERR_NONFINITE (out still written)
+ * if x held NaN/inf. */
+int ts_score_host(const ts_model *model, const float *x, int64_t n, int64_t f,
+                  double *out);
+
+void ts_free(ts_model *model);
+
+/* Thread-local message for the last failing call on this thread. */
+const char *ts_last_error(void);
+
+/* Number of scoring-kernel launches issued by this process so far. */
+int64_t ts_launch_count(void);
+
+/* Synthetic instances (BASELINE configs 3/4): fills rows [row0, row0+n) of a
+ * counter-based uniform [0,1) matrix in place on the current device, with
+ * entries zeroed with probability zero_prob.  Element e = row*f + col takes
+ * u = splitmix64(seed + (e+1)*0x9E3779B97F4A7C15) >> 40, scaled by 2^-24
+ * (reproducible on the host).  Not part of the reference interface. */
+int ts_synth_uniform(float *x, int64_t n, int64_t f, int64_t ld, uint64_t seed,
+                     int64_t row0, double zero_prob, void *stream);
+
+/* Library version string, e.g. "0.1.0 sm_100a". */
+const char *ts_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TREESCORE_GPU_H */

@@ -1,0 +1,222 @@
+// ts_capi.cpp -- the C ABI (include/treescore_gpu.h): argument checks that
+// mirror the reference's Evaluator errors (ref evaluators.py:204-220), the
+// per-segment launch sequence, and the host-buffer pipeline that stands in
+// for the reference's generated score_batch (ref codegen.py:115-121).
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <atomic>
+#include <string>
+
+#include "ts_internal.h"
+
+namespace ts {
+
+static thread_local std::string g_err;
+static std::atomic<long long> g_launches{0};
+
+void set_error(const std::string &msg) { g_err = msg; }
+
+int fail(int code, const std::string &msg) {
+    g_err = msg;
+    return code;
+}
+
+int cuda_fail(cudaError_t err, const char *what) {
+    char buf[512];
+    snprintf(buf, sizeof buf, "%s: %s (%s)", what, cudaGetErrorString(err), cudaGetErrorName(err));
+    g_err = buf;
+    return TS_ERR_CUDA;
+}
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+void free_tables(DeviceTables *t);
+
+namespace {
+
+struct DeviceGuard {
+    int prev = -1;
+    cudaError_t err = cudaSuccess;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) err = cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+int score_device(const ts_model *m, const float *x, int64_t n, int64_t f, int64_t ld,
+                 double *out, uint16_t *ord, int64_t ld_ord, int32_t *status,
+                 cudaStream_t stream) {
+    if (n == 0) return TS_OK;
+    ScoreArgs a{};
+    a.x = x;
+    a.n = n;
+    a.ld = ld;
+    a.F = m->num_features;
+    a.nodes = m->dev.nodes;
+    a.leaves = m->dev.leaves;
+    a.node_base = m->dev.node_base;
+    a.leaf_base = m->dev.leaf_base;
+    a.depth = m->dev.depth;
+    a.weight = m->dev.weight;
+    a.unit_w = m->unit_weights ? 1 : 0;
+    a.out = out;
+    a.ord = ord;
+    a.ld_ord = ld_ord;
+    a.status = status;
+    for (size_t s = 0; s < m->segments.size(); s++) {
+        const Segment &seg = m->segments[s];
+        a.t0 = seg.t0;
+        a.t1 = seg.t1;
+        a.accumulate = s > 0;
+        // Only the first launch of a call needs to flag non-finite input.
+        a.status = s == 0 ? status : nullptr;
+        cudaError_t e = launch_segment(seg, a, m->device, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "scoring kernel launch");
+    }
+    return TS_OK;
+}
+
+int check_args(const ts_model *m, const float *x, int64_t n, int64_t f, int64_t ld,
+               const double *out) {
+    if (!m) return fail(TS_ERR_INVALID, "model is NULL");
+    if (n < 0) return fail(TS_ERR_SHAPE, "n must be >= 0");
+    if (f != m->num_features) {
+        char buf[160];
+        snprintf(buf, sizeof buf, "dataset has shape (%lld, %lld), expected (n, %d)",
+                 (long long)n, (long long)f, m->num_features);
+        return fail(TS_ERR_SHAPE, buf);
+    }
+    if (ld < f) return fail(TS_ERR_SHAPE, "ld must be >= f");
+    if (n > 0 && (!x || !out)) return fail(TS_ERR_INVALID, "x/out is NULL");
+    return TS_OK;
+}
+
+}  // namespace
+}  // namespace ts
+
+using namespace ts;
+
+extern "C" int ts_model_get_info(const ts_model *m, ts_model_info *info) {
+    if (!m || !info) return fail(TS_ERR_INVALID, "NULL argument");
+    *info = m->info;
+    return TS_OK;
+}
+
+extern "C" int ts_score(const ts_model *m, const float *x, int64_t n, int64_t f, int64_t ld,
+                        double *out, uint16_t *ord_out, int64_t ld_ord, int32_t *status,
+                        void *stream) {
+    int rc = check_args(m, x, n, f, ld, out);
+    if (rc) return rc;
+    if (ord_out && ld_ord < n) return fail(TS_ERR_SHAPE, "ld_ord must be >= n");
+    DeviceGuard g(m->device);
+    if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
+    return score_device(m, x, n, f, ld, out, ord_out, ld_ord, status, (cudaStream_t)stream);
+}
+
+extern "C" int ts_score_host(const ts_model *mc, const float *x, int64_t n, int64_t f,
+                             double *out) {
+    int rc = check_args(mc, x, n, f, f, out);
+    if (rc) return rc;
+    if (n == 0) return TS_OK;
+    ts_model *m = const_cast<ts_model *>(mc);
+    DeviceGuard g(m->device);
+    if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
+    std::lock_guard<std::mutex> lock(m->scratch_mu);
+    HostScratch &s = m->scratch;
+    // Chunk so that H2D of chunk i+1 overlaps the scoring of chunk i.
+    const int64_t row_bytes = f * (int64_t)sizeof(float);
+    int64_t chunk = std::max<int64_t>(4096, (64ll << 20) / row_bytes);
+    chunk = std::min(chunk, n);
+    cudaError_t e = cudaSuccess;
+    if (!s.copy) {
+        if ((e = cudaStreamCreateWithFlags(&s.copy, cudaStreamNonBlocking)) ||
+            (e = cudaStreamCreateWithFlags(&s.compute, cudaStreamNonBlocking)))
+            return cuda_fail(e, "cudaStreamCreate");
+        for (int i = 0; i < 2; i++) {
+            if ((e = cudaEventCreateWithFlags(&s.copied[i], cudaEventDisableTiming)) ||
+                (e = cudaEventCreateWithFlags(&s.consumed[i], cudaEventDisableTiming)))
+                return cuda_fail(e, "cudaEventCreate");
+        }
+        if ((e = cudaMalloc(&s.status, sizeof(int32_t)))) return cuda_fail(e, "cudaMalloc");
+    }
+    if (s.x_rows < chunk) {
+        for (int i = 0; i < 2; i++) {
+            cudaFree(s.x[i]);
+            s.x[i] = nullptr;
+            if ((e = cudaMalloc(&s.x[i], chunk * row_bytes))) return cuda_fail(e, "cudaMalloc(x)");
+        }
+        s.x_rows = chunk;
+    }
+    if (s.out_rows < chunk) {
+        cudaFree(s.out);
+        s.out = nullptr;
+        if ((e = cudaMalloc(&s.out, 2 * chunk * sizeof(double))))
+            return cuda_fail(e, "cudaMalloc(out)");
+        s.out_rows = chunk;
+    }
+    if ((e = cudaMemsetAsync(s.status, 0, sizeof(int32_t), s.compute)))
+        return cuda_fail(e, "cudaMemsetAsync");
+    // The compute stream must not start before the status reset; the copy
+    // stream's first wait below orders buffer reuse.
+    int k = 0;
+    for (int64_t r0 = 0; r0 < n; r0 += chunk, k ^= 1) {
+        const int64_t rows = std::min(chunk, n - r0);
+        if ((e = cudaStreamWaitEvent(s.copy, s.consumed[k], 0)) ||
+            (e = cudaMemcpyAsync(s.x[k], x + r0 * f, rows * row_bytes, cudaMemcpyHostToDevice,
+                                 s.copy)) ||
+            (e = cudaEventRecord(s.copied[k], s.copy)) ||
+            (e = cudaStreamWaitEvent(s.compute, s.copied[k], 0)))
+            return cuda_fail(e, "host pipeline (H2D)");
+        double *dout = s.out + k * chunk;
+        rc = score_device(m, s.x[k], rows, f, f, dout, nullptr, 0, s.status, s.compute);
+        if (rc) return rc;
+        if ((e = cudaEventRecord(s.consumed[k], s.compute)) ||
+            (e = cudaMemcpyAsync(out + r0, dout, rows * sizeof(double), cudaMemcpyDeviceToHost,
+                                 s.compute)))
+            return cuda_fail(e, "host pipeline (D2H)");
+    }
+    int32_t flag = 0;
+    if ((e = cudaMemcpyAsync(&flag, s.status, sizeof(int32_t), cudaMemcpyDeviceToHost,
+                             s.compute)) ||
+        (e = cudaStreamSynchronize(s.compute)))
+        return cuda_fail(e, "host pipeline (sync)");
+    if (flag) return fail(TS_ERR_NONFINITE, "dataset contains non-finite values");
+    return TS_OK;
+}
+
+extern "C" void ts_free(ts_model *m) {
+    if (!m) return;
+    {
+        DeviceGuard g(m->device);
+        free_tables(&m->dev);
+        HostScratch &s = m->scratch;
+        if (s.copy) {
+            cudaStreamSynchronize(s.copy);
+            cudaStreamSynchronize(s.compute);
+        }
+        cudaFree(s.x[0]);
+        cudaFree(s.x[1]);
+        cudaFree(s.out);
+        cudaFree(s.status);
+        for (int i = 0; i < 2; i++) {
+            if (s.copied[i]) cudaEventDestroy(s.copied[i]);
+            if (s.consumed[i]) cudaEventDestroy(s.consumed[i]);
+        }
+        if (s.copy) cudaStreamDestroy(s.copy);
+        if (s.compute) cudaStreamDestroy(s.compute);
+    }
+    delete m;
+}
+
+extern "C" const char *ts_last_error(void) { return g_err.c_str(); }
+
+extern "C" int64_t ts_launch_count(void) { return g_launches.load(); }
+
+extern "C" const char *ts_version(void) { return "0.1.0 sm_100a"; }

@@ -1,0 +1,300 @@
+// ts_pack.cpp -- native node-table packer (replaces the reference's per-tree
+// Python recursion expand_to_complete, ref model.py:315-349, and the
+// VPredicatedEvaluator build, ref evaluators.py:490-512).
+//
+// Input: the flat logical model of include/treescore_gpu.h.  Output: device
+// tables in one of two layouts (ts_internal.h) plus the segment list the
+// scorer launches in tree order.  Validation mirrors the reference's model
+// checks (ref model.py:100-119 node values, :143-175 tree shape,
+// :197-220 ensemble, :538-602 parser graph checks) so that a model the
+// reference rejects is rejected here with the same class of error.
+#include <math.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "ts_internal.h"
+
+namespace ts {
+namespace {
+
+struct TreeShape {
+    int depth = 0;
+    bool complete = false;
+    std::vector<int32_t> bfs;    // logical ids in BFS order
+    std::vector<int32_t> level;  // depth of each logical id
+};
+
+std::string tree_msg(int t, const char *what) {
+    char buf[256];
+    snprintf(buf, sizeof buf, "tree %d: %s", t, what);
+    return buf;
+}
+
+// Structure check + depth.  Returns TS_OK or an error code (message set).
+int analyse_tree(const ts_model_desc *d, int t, TreeShape *s) {
+    const int64_t o = d->tree_node_offset[t];
+    const int64_t n64 = d->tree_node_offset[t + 1] - o;
+    if (n64 <= 0) return fail(TS_ERR_INVALID, tree_msg(t, "empty tree block"));
+    if (n64 > (int64_t)1 << 30) return fail(TS_ERR_INVALID, tree_msg(t, "too many nodes"));
+    const int32_t n = (int32_t)n64;
+    const int32_t *fid = d->node_fid + o;
+    const float *val = d->node_value + o;
+    const int32_t *lc = d->node_left + o;
+    const int32_t *rc = d->node_right + o;
+    std::vector<uint8_t> parents(n, 0);
+    for (int32_t i = 0; i < n; i++) {
+        if (!isfinite(val[i]))
+            return fail(TS_ERR_INVALID, tree_msg(t, fid[i] < 0 ? "leaf value must be finite"
+                                                               : "threshold must be finite"));
+        if (fid[i] < -1) return fail(TS_ERR_INVALID, tree_msg(t, "feature id must be non-negative"));
+        if (fid[i] < 0) continue;
+        if (fid[i] >= d->num_features)
+            return fail(TS_ERR_INVALID, tree_msg(t, "feature id out of range"));
+        for (int32_t c : {lc[i], rc[i]}) {
+            if (c < 0 || c >= n) return fail(TS_ERR_INVALID, tree_msg(t, "dangling child id"));
+            if (c == 0) return fail(TS_ERR_INVALID, tree_msg(t, "root must not appear as a child"));
+            if (++parents[c] > 1) return fail(TS_ERR_INVALID, tree_msg(t, "node has multiple parents"));
+        }
+    }
+    s->bfs.clear();
+    s->bfs.reserve(n);
+    s->level.assign(n, -1);
+    s->bfs.push_back(0);
+    s->level[0] = 0;
+    int depth = 0, leaves = 0;
+    for (size_t h = 0; h < s->bfs.size(); h++) {
+        int32_t i = s->bfs[h];
+        if (fid[i] < 0) {
+            leaves++;
+            depth = std::max(depth, (int)s->level[i]);
+            continue;
+        }
+        for (int32_t c : {lc[i], rc[i]}) {
+            if (s->level[c] >= 0) return fail(TS_ERR_INVALID, tree_msg(t, "cycle in tree"));
+            s->level[c] = s->level[i] + 1;
+            s->bfs.push_back(c);
+        }
+    }
+    if ((int32_t)s->bfs.size() != n)
+        return fail(TS_ERR_INVALID, tree_msg(t, "node unreachable from the root"));
+    if (depth > TS_MAX_DEPTH) {
+        char buf[160];
+        snprintf(buf, sizeof buf, "tree %d: depth %d exceeds MAX_DEPTH=%d for complete-table "
+                 "layouts", t, depth, TS_MAX_DEPTH);
+        return fail(TS_ERR_DEPTH, buf);
+    }
+    s->depth = depth;
+    s->complete = (int64_t)n == ((int64_t)1 << (depth + 1)) - 1 && leaves == (1 << depth);
+    return TS_OK;
+}
+
+// Heap fill of the complete expansion (same slot algebra as the reference:
+// children of slot i at 2i+1 and 2i+2; early leaves become dummy subtrees).
+void fill_complete(const int32_t *fid, const float *val, const int32_t *lc, const int32_t *rc,
+                   int depth, uint2 *nodes, float *leaves) {
+    const uint32_t n_int = (1u << depth) - 1u;
+    // Iterative level walk: src[k] = logical node occupying slot base+k.
+    std::vector<int32_t> src(1, 0), nxt;
+    for (int l = 0; l < depth; l++) {
+        const uint32_t base = (1u << l) - 1u;
+        nxt.resize(src.size() * 2);
+        for (size_t k = 0; k < src.size(); k++) {
+            int32_t i = src[k];
+            uint2 rec;
+            if (fid[i] < 0) {           // dummy: fid 0, theta +inf
+                rec.x = 0u;
+                float inf = INFINITY;
+                memcpy(&rec.y, &inf, 4);
+                nxt[2 * k] = i;
+                nxt[2 * k + 1] = i;
+            } else {
+                rec.x = (uint32_t)fid[i];
+                memcpy(&rec.y, &val[i], 4);
+                nxt[2 * k] = lc[i];
+                nxt[2 * k + 1] = rc[i];
+            }
+            nodes[base + k] = rec;
+        }
+        src.swap(nxt);
+    }
+    (void)n_int;
+    for (size_t k = 0; k < src.size(); k++) leaves[k] = val[src[k]];
+}
+
+// Compact BFS layout with adjacent sibling pairs and self-loop leaves.
+void fill_compact(const int32_t *fid, const float *val, const int32_t *lc, const int32_t *rc,
+                  const TreeShape &s, int F, uint2 *nodes) {
+    const int32_t n = (int32_t)s.bfs.size();
+    std::vector<int32_t> newid(n, -1);
+    std::vector<int32_t> order;
+    order.reserve(n);
+    order.push_back(0);
+    newid[0] = 0;
+    for (size_t h = 0; h < order.size(); h++) {
+        int32_t i = order[h];
+        if (fid[i] < 0) continue;
+        newid[lc[i]] = (int32_t)order.size();
+        order.push_back(lc[i]);
+        newid[rc[i]] = (int32_t)order.size();
+        order.push_back(rc[i]);
+    }
+    for (int32_t k = 0; k < n; k++) {
+        int32_t i = order[k];
+        uint2 rec;
+        memcpy(&rec.y, &val[i], 4);
+        if (fid[i] < 0) rec.x = (uint32_t)F | ((uint32_t)k << 16);
+        else rec.x = (uint32_t)fid[i] | ((uint32_t)newid[lc[i]] << 16);
+        nodes[k] = rec;
+    }
+}
+
+template <class T>
+int upload(T **dptr, const std::vector<T> &h) {
+    size_t bytes = std::max<size_t>(1, h.size()) * sizeof(T);
+    cudaError_t e = cudaMalloc((void **)dptr, bytes);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(model tables)");
+    if (!h.empty()) {
+        e = cudaMemcpy(*dptr, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpy(model tables)");
+    }
+    return TS_OK;
+}
+
+}  // namespace
+
+void free_tables(DeviceTables *t) {
+    cudaFree(t->nodes);
+    cudaFree(t->leaves);
+    cudaFree(t->node_base);
+    cudaFree(t->leaf_base);
+    cudaFree(t->depth);
+    cudaFree(t->weight);
+    *t = DeviceTables{};
+}
+
+}  // namespace ts
+
+extern "C" int ts_pack(const ts_model_desc *d, int device, ts_model **out) {
+    using namespace ts;
+    if (!out) return fail(TS_ERR_INVALID, "out is NULL");
+    *out = nullptr;
+    if (!d || !d->tree_node_offset || !d->tree_weight || !d->node_fid || !d->node_value ||
+        !d->node_left || !d->node_right)
+        return fail(TS_ERR_INVALID, "model description has NULL arrays");
+    if (d->num_features < 1) return fail(TS_ERR_INVALID, "num_features must be positive");
+    if (d->num_trees < 1) return fail(TS_ERR_INVALID, "ensemble must contain at least one tree");
+    if (d->tree_node_offset[0] != 0) return fail(TS_ERR_INVALID, "tree_node_offset[0] must be 0");
+    const int T = d->num_trees, F = d->num_features;
+    // Compact records hold fid and the sentinel row F in 16 bits.
+    const bool compact_ok_f = F <= 65534;
+
+    std::vector<TreeShape> shapes(T);
+    std::vector<int> layout(T);
+    int64_t n_nodes = 0, n_leaves = 0, sum_depth = 0, entries = 0;
+    int max_depth = 0, n_complete = 0, n_compact = 0;
+    bool unit = true;
+    for (int t = 0; t < T; t++) {
+        if (!isfinite(d->tree_weight[t]))
+            return fail(TS_ERR_INVALID, tree_msg(t, "tree weight must be finite"));
+        if (d->tree_weight[t] != 1.0) unit = false;
+        int rc = analyse_tree(d, t, &shapes[t]);
+        if (rc) return rc;
+        const TreeShape &s = shapes[t];
+        const int64_t nn = (int64_t)s.bfs.size();
+        if (s.complete || !compact_ok_f || nn > 65535) {
+            layout[t] = kComplete;
+            n_nodes += ((int64_t)1 << s.depth) - 1;
+            n_leaves += (int64_t)1 << s.depth;
+            n_complete++;
+        } else {
+            layout[t] = kCompact;
+            n_nodes += nn;
+            n_compact++;
+        }
+        sum_depth += s.depth;
+        entries += ((int64_t)1 << (s.depth + 1)) - 1;
+        max_depth = std::max(max_depth, s.depth);
+    }
+    if (n_nodes >= ((int64_t)1 << 32) || n_leaves >= ((int64_t)1 << 32))
+        return fail(TS_ERR_UNSUPPORTED, "packed tables exceed 2^32 records");
+
+    std::vector<uint2> nodes(n_nodes);
+    std::vector<float> leaves(n_leaves);
+    std::vector<uint32_t> node_base(T), leaf_base(T);
+    std::vector<int32_t> depth(T);
+    std::vector<double> weight(d->tree_weight, d->tree_weight + T);
+    int64_t np = 0, lp = 0;
+    for (int t = 0; t < T; t++) {
+        const int64_t o = d->tree_node_offset[t];
+        const int32_t *fid = d->node_fid + o;
+        const float *val = d->node_value + o;
+        const int32_t *lc = d->node_left + o;
+        const int32_t *rcc = d->node_right + o;
+        node_base[t] = (uint32_t)np;
+        leaf_base[t] = (uint32_t)lp;
+        depth[t] = shapes[t].depth;
+        if (layout[t] == kComplete) {
+            fill_complete(fid, val, lc, rcc, shapes[t].depth, nodes.data() + np, leaves.data() + lp);
+            np += ((int64_t)1 << shapes[t].depth) - 1;
+            lp += (int64_t)1 << shapes[t].depth;
+        } else {
+            fill_compact(fid, val, lc, rcc, shapes[t], F, nodes.data() + np);
+            np += (int64_t)shapes[t].bfs.size();
+        }
+    }
+
+    ts_model *m = new ts_model();
+    m->device = device;
+    m->num_features = F;
+    m->num_trees = T;
+    m->unit_weights = unit;
+    for (int t = 0; t < T; t++) {
+        int key_depth = layout[t] == kComplete ? shapes[t].depth : -1;
+        if (!m->segments.empty()) {
+            Segment &b = m->segments.back();
+            if (b.layout == layout[t] && (b.layout == kCompact || b.depth == key_depth)) {
+                b.t1 = t + 1;
+                continue;
+            }
+        }
+        m->segments.push_back(Segment{layout[t], layout[t] == kComplete ? key_depth : max_depth,
+                                      t, t + 1});
+    }
+    int prev = -1;
+    cudaGetDevice(&prev);
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) {
+        delete m;
+        return cuda_fail(e, "cudaSetDevice");
+    }
+    int rc = upload(&m->dev.nodes, nodes);
+    if (!rc) rc = upload(&m->dev.leaves, leaves);
+    if (!rc) rc = upload(&m->dev.node_base, node_base);
+    if (!rc) rc = upload(&m->dev.leaf_base, leaf_base);
+    if (!rc) rc = upload(&m->dev.depth, depth);
+    if (!rc) rc = upload(&m->dev.weight, weight);
+    if (prev >= 0) cudaSetDevice(prev);
+    if (rc) {
+        free_tables(&m->dev);
+        delete m;
+        return rc;
+    }
+    ts_model_info &info = m->info;
+    info.num_features = F;
+    info.num_trees = T;
+    info.max_depth = max_depth;
+    info.num_segments = (int32_t)m->segments.size();
+    info.sum_depth = sum_depth;
+    info.table_entries = entries;
+    info.device_bytes = n_nodes * 8 + n_leaves * 4 + (int64_t)T * (4 + 4 + 4 + 8);
+    info.complete_trees = n_complete;
+    info.compact_trees = n_compact;
+    info.device = device;
+    info.unit_weights = unit ? 1 : 0;
+    *out = m;
+    return TS_OK;
+}

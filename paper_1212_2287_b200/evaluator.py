@@ -1,0 +1,265 @@
+"""GPU evaluator: the reference's ``Evaluator`` interface over the C ABI.
+
+Mirrors ref ``treescore/evaluators.py``:
+
+* ``build(ensemble, kind, batch_size=None)`` (ref :565-585) -- here the kinds
+  are the GPU strategies; ``build_gpu`` is the direct constructor, the way
+  the reference builds its native strategy through ``build_generated``
+  (ref codegen.py:247-253) because ``StrategyKind`` is closed.
+* ``Evaluator.predict(x)`` / ``predict_batch(data)`` / ``_predict_into``
+  (ref :187-231) with the same ``ValueError`` messages for shape mismatch
+  (ref :204-220); ``stored_node_count`` (ref :197-200) counts complete-table
+  entries like the predicated kinds (ref :548-550).
+* ``leaf_indices(data)`` returns the per-tree predicated leaf ordinals --
+  what ``batch_kernel`` / ``leaf_index_predicated`` compute per tree
+  (ref :90-99, :122-134).
+
+Host side is PyTorch (device buffers, the current CUDA stream); all scoring
+runs in ``_ts_gpu.so``.  Inputs may be a ``Dataset``, anything numpy can view
+as float32, or a torch tensor on the CPU or on the evaluator's GPU.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import enum
+
+import numpy as np
+
+from . import _lib
+from .data import Dataset
+from .model import DepthLimitError, Ensemble, FlatModel, ModelSemanticError
+
+
+class StrategyKind(enum.Enum):
+    """GPU strategies (the reference's enum is closed, ref evaluators.py:56-68)."""
+
+    GPU_VPREDICATED = "gpu_vpredicated"
+
+    def __str__(self):
+        return self.value
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _ptr(a) -> ctypes.c_void_p:
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+class GpuModel:
+    """Packed device tables of one ensemble on one GPU (``ts_pack``)."""
+
+    def __init__(self, model, device: int | None = None):
+        torch = _torch()
+        if not torch.cuda.is_available():
+            raise _lib.NativeLibraryError("no CUDA device: the GPU scorer has no CPU fallback")
+        lib = _lib.load()
+        flat = model.flat() if isinstance(model, Ensemble) else model
+        if not isinstance(flat, FlatModel):
+            raise TypeError("model must be an Ensemble or a FlatModel")
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        arrs = [np.ascontiguousarray(flat.tree_off, np.int64),
+                np.ascontiguousarray(flat.weight, np.float64),
+                np.ascontiguousarray(flat.fid, np.int32),
+                np.ascontiguousarray(flat.value, np.float32),
+                np.ascontiguousarray(flat.left, np.int32),
+                np.ascontiguousarray(flat.right, np.int32)]
+        desc = _lib.ModelDesc(int(flat.num_features), int(flat.num_trees),
+                              *[a.ctypes.data for a in arrs])
+        handle = ctypes.c_void_p()
+        rc = lib.ts_pack(ctypes.byref(desc), self.device, ctypes.byref(handle))
+        if rc == _lib.TS_ERR_DEPTH:
+            raise DepthLimitError(_lib.last_error())
+        if rc == _lib.TS_ERR_INVALID:
+            raise ModelSemanticError(_lib.last_error())
+        if rc != _lib.TS_OK:
+            raise RuntimeError(f"ts_pack failed ({rc}): {_lib.last_error()}")
+        self._lib = lib
+        self.handle = handle
+        info = _lib.ModelInfo()
+        lib.ts_model_get_info(handle, ctypes.byref(info))
+        self.info = info.as_dict()
+        self.num_features = int(flat.num_features)
+        self.num_trees = int(flat.num_trees)
+
+    def score(self, x, out=None, ordinals=None, status=None, stream=None):
+        """Enqueue scoring of a CUDA float32 ``[n, f]`` tensor (row stride >= f).
+
+        ``out``: f64 CUDA tensor ``[n]`` (allocated if None).  ``ordinals``:
+        optional uint16-compatible CUDA tensor ``[T, >= n]`` (torch.int16 or
+        torch.uint16) receiving predicated leaf ordinals.  ``status``: optional
+        int32 CUDA scalar OR-ed with 1 on non-finite input.  Returns ``out``.
+        Stream-ordered on ``stream`` (default: torch's current stream).
+        """
+        torch = _torch()
+        if x.dim() != 2 or x.dtype != torch.float32 or not x.is_cuda:
+            raise TypeError("x must be a 2-D float32 CUDA tensor")
+        if x.stride(1) != 1:
+            raise ValueError("x rows must be contiguous (stride(1) == 1)")
+        n, f = x.shape
+        if f != self.num_features:
+            raise ValueError(f"dataset has shape {tuple(x.shape)}, expected (n, {self.num_features})")
+        if out is None:
+            out = torch.empty(n, dtype=torch.float64, device=x.device)
+        ld_ord = 0
+        ord_ptr = None
+        if ordinals is not None:
+            if ordinals.element_size() != 2 or ordinals.dim() != 2 or ordinals.stride(1) != 1 \
+                    or ordinals.shape[0] != self.num_trees or ordinals.shape[1] < n:
+                raise ValueError("ordinals must be a [T, >=n] 16-bit row-major tensor")
+            ld_ord = ordinals.stride(0)
+            ord_ptr = ctypes.c_void_p(ordinals.data_ptr())
+        if stream is None:
+            stream = torch.cuda.current_stream(x.device)
+        rc = self._lib.ts_score(self.handle, ctypes.c_void_p(x.data_ptr()), n, f, x.stride(0),
+                                ctypes.c_void_p(out.data_ptr()), ord_ptr, ld_ord,
+                                ctypes.c_void_p(status.data_ptr()) if status is not None else None,
+                                ctypes.c_void_p(stream.cuda_stream))
+        if rc != _lib.TS_OK:
+            raise RuntimeError(f"ts_score failed ({rc}): {_lib.last_error()}")
+        return out
+
+    def score_host(self, matrix: np.ndarray, out: np.ndarray) -> None:
+        """``ts_score_host``: host fp32 ``[n, f]`` -> host f64 ``[n]``."""
+        rc = self._lib.ts_score_host(self.handle, _ptr(matrix), matrix.shape[0],
+                                     matrix.shape[1], _ptr(out))
+        if rc == _lib.TS_ERR_NONFINITE:
+            raise ValueError("dataset contains non-finite values")
+        if rc == _lib.TS_ERR_SHAPE:
+            raise ValueError(_lib.last_error())
+        if rc != _lib.TS_OK:
+            raise RuntimeError(f"ts_score_host failed ({rc}): {_lib.last_error()}")
+
+    def close(self):
+        if getattr(self, "handle", None) is not None and self.handle.value:
+            self._lib.ts_free(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 - interpreter shutdown
+            pass
+
+
+class GpuEvaluator:
+    """Immutable GPU scoring strategy built from an ensemble.
+
+    ``predict`` / ``predict_batch`` return exactly the reference's f64 scores
+    (bit-identical: same tie rule, dummy routing, fp32 tables, f64 tree-order
+    multiply-then-add).  Non-finite inputs raise ``ValueError`` (the
+    reference's ``Dataset`` contract, ref data.py:50-51); there is no silent
+    NaN routing.
+    """
+
+    kind = StrategyKind.GPU_VPREDICATED
+
+    def __init__(self, ensemble, batch_size: int | None = None, device: int | None = None):
+        if batch_size is not None:
+            batch_size = int(batch_size)
+            if batch_size < 1:
+                raise ValueError(f"batch_size must be >= 1, got {batch_size}")
+        self.batch_size = batch_size
+        self.model = GpuModel(ensemble, device)
+        self.num_features = self.model.num_features
+        self.num_trees = self.model.num_trees
+        self.device = self.model.device
+
+    # -- reference-compatible surface ---------------------------------------------
+
+    def predict(self, x) -> float:
+        x = np.ascontiguousarray(x, dtype=np.float32)
+        if x.ndim != 1 or x.shape[0] != self.num_features:
+            raise ValueError(f"feature vector has shape {x.shape}, expected ({self.num_features},)")
+        return float(self.predict_batch(x[None, :])[0])
+
+    def predict_batch(self, data) -> np.ndarray:
+        torch = _torch()
+        if isinstance(data, torch.Tensor):
+            return self._predict_tensor(data).cpu().numpy()
+        matrix = self._coerce_matrix(data)
+        out = np.empty(matrix.shape[0], dtype=np.float64)
+        self._predict_into(matrix, out)
+        return out
+
+    def _predict_into(self, matrix, out) -> None:
+        if matrix.shape[0] == 0:
+            return
+        if out.dtype != np.float64 or not out.flags.c_contiguous:
+            raise ValueError("out must be a C-contiguous float64 array")
+        self.model.score_host(np.ascontiguousarray(matrix, dtype=np.float32), out)
+
+    def _coerce_matrix(self, data) -> np.ndarray:
+        matrix = data.matrix if isinstance(data, Dataset) else np.ascontiguousarray(
+            data, dtype=np.float32)
+        if matrix.ndim != 2 or matrix.shape[1] != self.num_features:
+            raise ValueError(f"dataset has shape {matrix.shape}, expected (n, {self.num_features})")
+        return matrix
+
+    @property
+    def stored_node_count(self) -> int:
+        return int(self.model.info["table_entries"])
+
+    # -- GPU-native extras ---------------------------------------------------------
+
+    def _predict_tensor(self, x):
+        torch = _torch()
+        if x.dim() != 2 or x.shape[1] != self.num_features:
+            raise ValueError(f"dataset has shape {tuple(x.shape)}, expected (n, {self.num_features})")
+        dev = torch.device("cuda", self.device)
+        x = x.to(device=dev, dtype=torch.float32)
+        if x.stride(1) != 1:
+            x = x.contiguous()
+        status = torch.zeros(1, dtype=torch.int32, device=dev)
+        out = self.model.score(x, status=status)
+        if int(status.item()):
+            raise ValueError("dataset contains non-finite values")
+        return out
+
+    def score_device(self, x, out=None, stream=None):
+        """Scores of a resident CUDA tensor, stream-ordered, no host sync."""
+        return self.model.score(x, out=out, stream=stream)
+
+    def leaf_indices(self, data) -> np.ndarray:
+        """Per-tree predicated leaf ordinals, shape ``(T, n)``, int64.
+
+        Row ``t`` equals the reference ``batch_kernel(d_t)`` result on
+        ``expand_to_complete(tree_t)`` (ref evaluators.py:90-99).
+        """
+        torch = _torch()
+        dev = torch.device("cuda", self.device)
+        if isinstance(data, torch.Tensor):
+            x = data.to(device=dev, dtype=torch.float32).contiguous()
+        else:
+            x = torch.from_numpy(self._coerce_matrix(data)).to(dev)
+        n = x.shape[0]
+        ords = torch.empty((self.num_trees, max(n, 1)), dtype=torch.int16, device=dev)
+        status = torch.zeros(1, dtype=torch.int32, device=dev)
+        if n:
+            self.model.score(x, ordinals=ords, status=status)
+        if int(status.item()):
+            raise ValueError("dataset contains non-finite values")
+        return ords[:, :n].cpu().numpy().view(np.uint16).astype(np.int64)
+
+    def close(self):
+        self.model.close()
+
+    def __repr__(self):
+        return f"GpuEvaluator(kind={self.kind}, trees={self.num_trees}, device={self.device})"
+
+
+def build_gpu(ensemble, batch_size: int | None = None, device: int | None = None) -> GpuEvaluator:
+    """Pack ``ensemble`` (Ensemble, FlatModel or reference treescore Ensemble)."""
+    if not isinstance(ensemble, (Ensemble, FlatModel)) and hasattr(ensemble, "trees"):
+        ensemble = Ensemble.from_reference(ensemble)
+    return GpuEvaluator(ensemble, batch_size, device)
+
+
+def build(ensemble, kind=StrategyKind.GPU_VPREDICATED, batch_size: int | None = None,
+          device: int | None = None) -> GpuEvaluator:
+    """``build`` with the reference's argument meaning and errors (ref :565-585)."""
+    kind = StrategyKind(kind)  # ValueError for unknown kinds, as in the reference
+    return build_gpu(ensemble, batch_size, device)

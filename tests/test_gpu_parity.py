@@ -1,0 +1,179 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's
+golden vectors and the pinned CPU oracle.  Scores must be bit-exact f64
+(same tie rule, dummy routing, fp32 tables and tree-order multiply-then-add);
+per-tree predicated leaf ordinals must be bit-exact."""
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import GOLDEN_CASES, has_cuda, load_golden
+
+pytestmark = [pytest.mark.gpu,
+              pytest.mark.skipif(not has_cuda(), reason="needs a CUDA device")]
+
+
+def _ev(model, **kw):
+    from paper_1212_2287_b200 import build_gpu
+    return build_gpu(model, **kw)
+
+
+@pytest.mark.parametrize("name", GOLDEN_CASES)
+def test_golden_scores_and_ordinals(name):
+    ens, g = load_golden(name)
+    ev = _ev(ens)
+    got = ev.predict_batch(g["X"])
+    assert np.array_equal(got, g["scores"])                       # bit-exact
+    ords = ev.leaf_indices(g["X"])
+    assert np.array_equal(ords, g["ordinals"])
+
+
+@pytest.mark.parametrize("name", GOLDEN_CASES)
+def test_golden_device_path_and_single_rows(name):
+    import torch
+    ens, g = load_golden(name)
+    ev = _ev(ens)
+    x = torch.from_numpy(g["X"]).cuda()
+    out = ev.score_device(x)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), g["scores"])
+    for i in range(min(5, g["X"].shape[0])):
+        assert ev.predict(g["X"][i]) == g["scores"][i]
+
+
+def test_strided_rows_and_tile_remainders():
+    import torch
+    ens, g = load_golden("complete_d6")
+    ev = _ev(ens)
+    X = g["X"]
+    for n in (1, 31, 33, 255, 417, 1023):
+        wide = torch.zeros((n, 140), dtype=torch.float32, device="cuda")
+        wide[:, :136] = torch.from_numpy(X[:n])
+        out = ev.score_device(wide[:, :136])   # row stride 140 > f
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy(), g["scores"][:n]), n
+
+
+def test_permutation_independence():
+    # ref tests/test_evaluators.py:159-169
+    ens, g = load_golden("mixed")
+    ev = _ev(ens)
+    perm = np.random.default_rng(0).permutation(g["X"].shape[0])
+    got = ev.predict_batch(g["X"][perm])
+    back = np.empty_like(got)
+    back[perm] = got
+    assert np.array_equal(back, g["scores"])
+
+
+def test_empty_input_and_shape_errors():
+    # ref tests/test_evaluators.py:119-125 (empty), :118-127 (mismatch)
+    ens, _ = load_golden("tie")
+    ev = _ev(ens)
+    assert ev.predict_batch(np.zeros((0, 1), np.float32)).shape == (0,)
+    with pytest.raises(ValueError, match="dataset"):
+        ev.predict_batch(np.zeros((3, 2), np.float32))
+    with pytest.raises(ValueError, match="feature vector"):
+        ev.predict(np.zeros(2, np.float32))
+
+
+def test_nonfinite_inputs_rejected():
+    ens, g = load_golden("complete_d6")
+    ev = _ev(ens)
+    for bad in (np.nan, np.inf, -np.inf):
+        X = g["X"][:100].copy()
+        X[57, 3] = bad
+        with pytest.raises(ValueError, match="non-finite"):
+            ev.predict_batch(X)
+
+
+def test_depth_limit_and_invalid_models():
+    # ref tests/test_evaluators.py:51-62: depth 17 -> DepthLimitError
+    from paper_1212_2287_b200 import DepthLimitError, Ensemble, Node, Tree
+    node = Node.leaf(1.0)
+    for level in range(17):
+        node = Node.internal(0, 0.5 / (level + 2), node, Node.leaf(2.0))
+    with pytest.raises(DepthLimitError):
+        _ev(Ensemble(2, [Tree(node)]))
+
+
+def test_weights_and_many_segments():
+    # alternating complete/irregular trees -> one launch per segment, f64
+    # accumulation carried across launches in tree order.
+    from paper_1212_2287_b200 import Ensemble
+    ens, g = load_golden("mixed")
+    trees = [(t, w * (1.0 + 0.25 * i)) for i, (t, w) in enumerate(ens.trees)]
+    ens2 = Ensemble(ens.num_features, trees)
+    ev = _ev(ens2)
+    assert ev.model.info["num_segments"] > 3
+    c = oracle.COracle(ens2.flat().arrays())
+    assert np.array_equal(ev.predict_batch(g["X"]), c.score(g["X"]))
+
+
+def test_config0_full_vs_oracle():
+    from paper_1212_2287_b200 import synth
+    w = synth.config0()
+    ev = _ev(w.flat)
+    c = oracle.COracle(w.flat.arrays())
+    ref, ref_ord = c.score(w.x, with_ordinals=True)
+    assert np.array_equal(ev.predict_batch(w.x), ref)
+    assert np.array_equal(ev.leaf_indices(w.x), ref_ord.astype(np.int64))
+
+
+def test_config1_ties_subsample_vs_oracle():
+    from paper_1212_2287_b200 import synth
+    w = synth.config1(n=60_000)
+    ev = _ev(w.flat)
+    c = oracle.COracle(w.flat.arrays())
+    ref, ref_ord = c.score(w.x, with_ordinals=True)
+    assert np.array_equal(ev.predict_batch(w.x), ref)
+    assert np.array_equal(ev.leaf_indices(w.x[:5000]), ref_ord[:, :5000].astype(np.int64))
+
+
+@pytest.mark.parametrize("depth", [3, 4, 6, 8, 10, 12])
+def test_config2_depths_vs_oracle(depth):
+    from paper_1212_2287_b200 import synth
+    w = synth.config2(depth, n=4096, trees=200)
+    ev = _ev(w.flat)
+    c = oracle.COracle(w.flat.arrays())
+    ref, ref_ord = c.score(w.x, with_ordinals=True)
+    assert np.array_equal(ev.predict_batch(w.x), ref)
+    assert np.array_equal(ev.leaf_indices(w.x), ref_ord.astype(np.int64))
+
+
+def test_config3_irregular_device_generated_rows():
+    import torch
+    from paper_1212_2287_b200 import synth, _lib
+    w = synth.config3(n=20_000, trees=300)
+    ev = _ev(w.flat)
+    x = torch.empty((w.n, w.f), dtype=torch.float32, device="cuda")
+    rc = _lib.load().ts_synth_uniform(x.data_ptr(), w.n, w.f, w.f, w.hash_seed, 0, w.zero_prob,
+                                      torch.cuda.current_stream().cuda_stream)
+    assert rc == 0
+    out = ev.score_device(x)
+    host = w.rows(0, w.n)
+    assert np.array_equal(x.cpu().numpy(), host)   # device generator == host
+    c = oracle.COracle(w.flat.arrays())
+    ref, ref_ord = c.score(host, with_ordinals=True)
+    assert np.array_equal(out.cpu().numpy(), ref)
+    assert np.array_equal(ev.leaf_indices(host[:3000]), ref_ord[:, :3000].astype(np.int64))
+
+
+def test_wide_features_global_path():
+    # F too wide for a shared-memory tile -> the global-read kernel variant.
+    from paper_1212_2287_b200 import synth
+    flat = synth.irregular_flat(77, 40, 3000, leaves=32)
+    X = np.random.default_rng(1).random((700, 3000), dtype=np.float32)
+    ev = _ev(flat)
+    c = oracle.COracle(flat.arrays())
+    ref, ref_ord = c.score(X, with_ordinals=True)
+    assert np.array_equal(ev.predict_batch(X), ref)
+    assert np.array_equal(ev.leaf_indices(X), ref_ord.astype(np.int64))
+
+
+def test_launch_counter_advances():
+    from paper_1212_2287_b200 import _lib
+    ens, g = load_golden("complete_d6")
+    ev = _ev(ens)
+    before = _lib.launch_count()
+    ev.predict_batch(g["X"])
+    assert _lib.launch_count() > before

@@ -1,0 +1,56 @@
+"""The C-ABI library builds, loads without a GPU, and exports every symbol
+include/treescore_gpu.h declares (no compute calls here)."""
+
+import os
+import re
+
+from paper_1212_2287_b200 import _lib
+from paper_1212_2287_b200.build import build
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_functions():
+    text = open(os.path.join(ROOT, "include", "treescore_gpu.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(ts_[a-z_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    build()
+    lib = _lib.load()
+    names = header_functions()
+    assert len(names) >= 8
+    for name in names:
+        assert hasattr(lib, name), name
+    assert set(names) == set(_lib.EXPORTS)
+    assert lib.ts_version().decode().endswith("sm_100a")
+
+
+def test_library_is_sm100a_only():
+    import subprocess
+    out = subprocess.run(["cuobjdump", "--list-elf", _lib.SO_PATH], capture_output=True,
+                         text=True).stdout
+    archs = set(re.findall(r"sm_\d+a?", out))
+    assert archs == {"sm_100a"}, archs
+
+
+def test_pack_rejects_bad_models_without_gpu():
+    # Validation happens before any device call, so it runs on the CPU.
+    import ctypes
+    import numpy as np
+    lib = _lib.load()
+    off = np.array([0, 3], np.int64)
+    w = np.array([1.0])
+    fid = np.array([5, -1, -1], np.int32)        # fid 5 >= num_features 2
+    val = np.array([0.5, 1, 2], np.float32)
+    lc = np.array([1, -1, -1], np.int32)
+    rc = np.array([2, -1, -1], np.int32)
+    desc = _lib.ModelDesc(2, 1, *[a.ctypes.data for a in (off, w, fid, val, lc, rc)])
+    h = ctypes.c_void_p()
+    assert lib.ts_pack(ctypes.byref(desc), 0, ctypes.byref(h)) == _lib.TS_ERR_INVALID
+    assert "out of range" in _lib.last_error()
+    fid[0] = 0
+    val[0] = np.inf
+    assert lib.ts_pack(ctypes.byref(desc), 0, ctypes.byref(h)) == _lib.TS_ERR_INVALID
+    assert "finite" in _lib.last_error()
