@@ -25,7 +25,7 @@ TS_ERR_UNSUPPORTED = 7
 
 # Every symbol include/treescore_gpu.h declares (checked by the CPU tests).
 EXPORTS = ("ts_pack", "ts_model_get_info", "ts_score", "ts_score_host", "ts_free",
-           "ts_last_error", "ts_launch_count", "ts_version", "ts_synth_uniform")
+           "ts_last_error", "ts_launch_count", "ts_version", "ts_synth_uniform", "ts_set_kernel_path")
 
 
 class NativeLibraryError(RuntimeError):
@@ -100,6 +100,8 @@ def load(build_if_missing: bool = True):
         lib.ts_synth_uniform.argtypes = [P, I64, I64, I64, ctypes.c_uint64, I64,
                                          ctypes.c_double, P]
         lib.ts_synth_uniform.restype = ctypes.c_int
+        lib.ts_set_kernel_path.argtypes = [ctypes.c_int]
+        lib.ts_set_kernel_path.restype = ctypes.c_int
         for name in EXPORTS:
             getattr(lib, name)
         _lib = lib

@@ -17,7 +17,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "_ts_gpu.so")
-SOURCES = ["ts_kernels.cu", "ts_synth.cu", "ts_pack.cpp", "ts_capi.cpp"]
+SOURCES = ["ts_kernels.cu", "ts_stream.cu", "ts_synth.cu", "ts_pack.cpp", "ts_capi.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

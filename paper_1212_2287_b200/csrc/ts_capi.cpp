@@ -15,6 +15,7 @@ namespace ts {
 
 static thread_local std::string g_err;
 static std::atomic<long long> g_launches{0};
+static int g_force_l1 = 0;
 
 void set_error(const std::string &msg) { g_err = msg; }
 
@@ -59,11 +60,10 @@ int score_device(const ts_model *m, const float *x, int64_t n, int64_t f, int64_
     a.n = n;
     a.ld = ld;
     a.F = m->num_features;
-    a.nodes = m->dev.nodes;
-    a.leaves = m->dev.leaves;
-    a.node_base = m->dev.node_base;
-    a.leaf_base = m->dev.leaf_base;
+    a.blob = m->dev.blob;
+    a.tree_off16 = m->dev.tree_off16;
     a.depth = m->dev.depth;
+    a.force_l1 = g_force_l1;
     a.weight = m->dev.weight;
     a.unit_w = m->unit_weights ? 1 : 0;
     a.out = out;
@@ -220,3 +220,9 @@ extern "C" const char *ts_last_error(void) { return g_err.c_str(); }
 extern "C" int64_t ts_launch_count(void) { return g_launches.load(); }
 
 extern "C" const char *ts_version(void) { return "0.1.0 sm_100a"; }
+
+extern "C" int ts_set_kernel_path(int path) {
+    if (path < 0 || path > 1) return fail(TS_ERR_INVALID, "path must be 0 (auto) or 1 (L1 only)");
+    g_force_l1 = path;
+    return TS_OK;
+}

@@ -31,16 +31,28 @@ struct Segment {
     int layout;   // Layout
     int depth;    // kComplete: the common depth of every tree in the segment
     int t0, t1;   // tree range [t0, t1) in evaluation order
+    uint64_t byte0;  // blob offset of tree t0
 };
 
+// All trees live in one byte blob, tree t at byte 16 * tree_off16[t]:
+//  kComplete: (2^d - 1) uint2 {fid << kFidShift, theta bits} in heap order, then 2^d fp32
+//             leaves, padded to 16 bytes (so a run of equal-depth trees is a
+//             regular array the TMA streams chunk by chunk);
+//  kCompact:  n_t uint2 records (see Layout), padded to 16 bytes.
 struct DeviceTables {
-    uint2 *nodes = nullptr;          // node records, all trees
-    float *leaves = nullptr;         // kComplete leaf values, all trees
-    uint32_t *node_base = nullptr;   // [T] first record of tree t
-    uint32_t *leaf_base = nullptr;   // [T] first leaf of tree t (kComplete)
+    unsigned char *blob = nullptr;
+    uint32_t *tree_off16 = nullptr;  // [T]
     int32_t *depth = nullptr;        // [T]
     double *weight = nullptr;        // [T]
 };
+
+// kComplete records store fid << kFidShift: the byte offset of feature fid's
+// row in the streaming kernel's 256-instance x tile (256 * 4 = 1 << 10).
+constexpr int kFidShift = 10;
+
+inline uint32_t complete_tree_bytes(int d) {
+    return (uint32_t)((((1u << d) - 1u) * 8u + (1u << d) * 4u + 15u) & ~15u);
+}
 
 struct HostScratch {
     float *x[2] = {nullptr, nullptr};
@@ -75,10 +87,8 @@ struct ScoreArgs {
     const float *x;
     long long n, ld;
     int F;
-    const uint2 *nodes;
-    const float *leaves;
-    const uint32_t *node_base;
-    const uint32_t *leaf_base;
+    const unsigned char *blob;
+    const uint32_t *tree_off16;
     const int32_t *depth;
     const double *weight;
     int t0, t1;
@@ -88,7 +98,32 @@ struct ScoreArgs {
     uint16_t *ord;
     long long ld_ord;
     int32_t *status;
+    int force_l1;  // testing: use the L1-path kernels even when streaming fits
 };
+
+// Arguments of the shared-memory streaming kernel (ts_stream.cu).
+constexpr int kStreamMaxDepth = 11;
+struct StreamArgs {
+    const float *x;
+    long long n, ld;
+    int F;
+    const unsigned char *blob;
+    unsigned long long seg_byte0;  // blob offset of tree t0
+    uint32_t tree_bytes;           // complete_tree_bytes(D)
+    int tpc;                       // trees per chunk
+    uint32_t chunk_cap;            // bytes per ring stage
+    uint32_t xs_bytes;             // instance tile bytes
+    const double *weight;
+    int t0, t1;
+    int unit_w;
+    int accumulate;
+    double *out;
+    uint16_t *ord;
+    long long ld_ord;
+    int32_t *status;
+};
+bool plan_stream(int F, int D, int device, StreamArgs *a);
+cudaError_t launch_stream(int D, const StreamArgs &a, int device, cudaStream_t stream);
 
 // Launch the kernel of one segment; returns cudaSuccess or the launch error.
 cudaError_t launch_segment(const Segment &seg, const ScoreArgs &args, int device,

@@ -118,7 +118,8 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_complete(ScoreArgs a) {
             uint32_t j[K];
 #pragma unroll
             for (int k = 0; k < K; k++) {
-                nd[k] = a.nodes + __ldg(a.node_base + t + k);
+                nd[k] = reinterpret_cast<const uint2 *>(a.blob +
+                                                        16ull * __ldg(a.tree_off16 + t + k));
                 j[k] = 0;
             }
 #pragma unroll
@@ -126,30 +127,32 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_complete(ScoreArgs a) {
 #pragma unroll
                 for (int k = 0; k < K; k++) {
                     const uint2 q = __ldg(nd[k] + j[k]);
-                    const float xv = XG ? __ldg(xr + q.x) : xr[q.x * xstride];
+                    const uint32_t fid = q.x >> kFidShift;
+                    const float xv = XG ? __ldg(xr + fid) : xr[fid * xstride];
                     j[k] = 2u * j[k] + 1u + (xv >= __uint_as_float(q.y) ? 1u : 0u);
                 }
             }
 #pragma unroll
             for (int k = 0; k < K; k++) {
                 const uint32_t ord = j[k] - ((1u << D) - 1u);
-                const float lv = __ldg(a.leaves + __ldg(a.leaf_base + t + k) + ord);
+                const float lv = __ldg(reinterpret_cast<const float *>(nd[k] + ((1u << D) - 1u)) + ord);
                 acc = a.unit_w ? __dadd_rn(acc, (double)lv)
                                : __dadd_rn(acc, __dmul_rn(__ldg(a.weight + t + k), (double)lv));
                 if (a.ord && valid) a.ord[(long long)(t + k) * a.ld_ord + row] = (uint16_t)ord;
             }
         }
         for (; t < a.t1; t++) {
-            const uint2 *nd = a.nodes + __ldg(a.node_base + t);
+            const uint2 *nd = reinterpret_cast<const uint2 *>(a.blob + 16ull * __ldg(a.tree_off16 + t));
             uint32_t j = 0;
 #pragma unroll
             for (int l = 0; l < D; l++) {
                 const uint2 q = __ldg(nd + j);
-                const float xv = XG ? __ldg(xr + q.x) : xr[q.x * xstride];
+                const uint32_t fid = q.x >> kFidShift;
+                const float xv = XG ? __ldg(xr + fid) : xr[fid * xstride];
                 j = 2u * j + 1u + (xv >= __uint_as_float(q.y) ? 1u : 0u);
             }
             const uint32_t ord = j - ((1u << D) - 1u);
-            const float lv = __ldg(a.leaves + __ldg(a.leaf_base + t) + ord);
+            const float lv = __ldg(reinterpret_cast<const float *>(nd + ((1u << D) - 1u)) + ord);
             acc = a.unit_w ? __dadd_rn(acc, (double)lv)
                            : __dadd_rn(acc, __dmul_rn(__ldg(a.weight + t), (double)lv));
             if (a.ord && valid) a.ord[(long long)t * a.ld_ord + row] = (uint16_t)ord;
@@ -194,7 +197,7 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_compact(ScoreArgs a) {
 #pragma unroll
             for (int k = 0; k < K; k++) {
                 const int tt = k < kk ? t + k : t;
-                nd[k] = a.nodes + __ldg(a.node_base + tt);
+                nd[k] = reinterpret_cast<const uint2 *>(a.blob + 16ull * __ldg(a.tree_off16 + tt));
                 dk[k] = __ldg(a.depth + tt);
                 dmax = max(dmax, dk[k]);
                 j[k] = 0;
@@ -269,6 +272,28 @@ const LaunchFn kCompleteTable[TS_MAX_DEPTH + 1] = {
 cudaError_t launch_segment(const Segment &seg, const ScoreArgs &args, int device,
                            cudaStream_t stream) {
     if (args.n <= 0) return cudaSuccess;
+    if (seg.layout == kComplete && !args.force_l1) {
+        StreamArgs sa{};
+        sa.tree_bytes = complete_tree_bytes(seg.depth);
+        if (plan_stream(args.F, seg.depth, device, &sa)) {
+            sa.x = args.x;
+            sa.n = args.n;
+            sa.ld = args.ld;
+            sa.F = args.F;
+            sa.blob = args.blob;
+            sa.seg_byte0 = seg.byte0;
+            sa.weight = args.weight;
+            sa.t0 = args.t0;
+            sa.t1 = args.t1;
+            sa.unit_w = args.unit_w;
+            sa.accumulate = args.accumulate;
+            sa.out = args.out;
+            sa.ord = args.ord;
+            sa.ld_ord = args.ld_ord;
+            sa.status = args.status;
+            return launch_stream(seg.depth, sa, device, stream);
+        }
+    }
     int optin = 0;
     cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
     if (e != cudaSuccess) return e;

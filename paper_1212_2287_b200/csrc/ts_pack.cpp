@@ -96,7 +96,6 @@ int analyse_tree(const ts_model_desc *d, int t, TreeShape *s) {
 // children of slot i at 2i+1 and 2i+2; early leaves become dummy subtrees).
 void fill_complete(const int32_t *fid, const float *val, const int32_t *lc, const int32_t *rc,
                    int depth, uint2 *nodes, float *leaves) {
-    const uint32_t n_int = (1u << depth) - 1u;
     // Iterative level walk: src[k] = logical node occupying slot base+k.
     std::vector<int32_t> src(1, 0), nxt;
     for (int l = 0; l < depth; l++) {
@@ -112,7 +111,7 @@ void fill_complete(const int32_t *fid, const float *val, const int32_t *lc, cons
                 nxt[2 * k] = i;
                 nxt[2 * k + 1] = i;
             } else {
-                rec.x = (uint32_t)fid[i];
+                rec.x = (uint32_t)fid[i] << kFidShift;
                 memcpy(&rec.y, &val[i], 4);
                 nxt[2 * k] = lc[i];
                 nxt[2 * k + 1] = rc[i];
@@ -121,7 +120,6 @@ void fill_complete(const int32_t *fid, const float *val, const int32_t *lc, cons
         }
         src.swap(nxt);
     }
-    (void)n_int;
     for (size_t k = 0; k < src.size(); k++) leaves[k] = val[src[k]];
 }
 
@@ -167,10 +165,8 @@ int upload(T **dptr, const std::vector<T> &h) {
 }  // namespace
 
 void free_tables(DeviceTables *t) {
-    cudaFree(t->nodes);
-    cudaFree(t->leaves);
-    cudaFree(t->node_base);
-    cudaFree(t->leaf_base);
+    cudaFree(t->blob);
+    cudaFree(t->tree_off16);
     cudaFree(t->depth);
     cudaFree(t->weight);
     *t = DeviceTables{};
@@ -194,7 +190,7 @@ extern "C" int ts_pack(const ts_model_desc *d, int device, ts_model **out) {
 
     std::vector<TreeShape> shapes(T);
     std::vector<int> layout(T);
-    int64_t n_nodes = 0, n_leaves = 0, sum_depth = 0, entries = 0;
+    int64_t sum_depth = 0, entries = 0;
     int max_depth = 0, n_complete = 0, n_compact = 0;
     bool unit = true;
     for (int t = 0; t < T; t++) {
@@ -207,43 +203,45 @@ extern "C" int ts_pack(const ts_model_desc *d, int device, ts_model **out) {
         const int64_t nn = (int64_t)s.bfs.size();
         if (s.complete || !compact_ok_f || nn > 65535) {
             layout[t] = kComplete;
-            n_nodes += ((int64_t)1 << s.depth) - 1;
-            n_leaves += (int64_t)1 << s.depth;
             n_complete++;
         } else {
             layout[t] = kCompact;
-            n_nodes += nn;
             n_compact++;
         }
         sum_depth += s.depth;
         entries += ((int64_t)1 << (s.depth + 1)) - 1;
         max_depth = std::max(max_depth, s.depth);
     }
-    if (n_nodes >= ((int64_t)1 << 32) || n_leaves >= ((int64_t)1 << 32))
-        return fail(TS_ERR_UNSUPPORTED, "packed tables exceed 2^32 records");
-
-    std::vector<uint2> nodes(n_nodes);
-    std::vector<float> leaves(n_leaves);
-    std::vector<uint32_t> node_base(T), leaf_base(T);
+    // Blob layout: tree t at 16 * tree_off16[t] (see DeviceTables).
+    std::vector<uint64_t> off(T + 1, 0);
+    for (int t = 0; t < T; t++) {
+        uint64_t bytes = layout[t] == kComplete
+                             ? complete_tree_bytes(shapes[t].depth)
+                             : ((uint64_t)shapes[t].bfs.size() * 8u + 15u) & ~(uint64_t)15u;
+        off[t + 1] = off[t] + bytes;
+    }
+    if (off[T] / 16 >= ((uint64_t)1 << 32))
+        return fail(TS_ERR_UNSUPPORTED, "packed tables exceed 64 GiB");
+    std::vector<unsigned char> blob(off[T], 0);
+    std::vector<uint32_t> off16(T);
     std::vector<int32_t> depth(T);
     std::vector<double> weight(d->tree_weight, d->tree_weight + T);
-    int64_t np = 0, lp = 0;
     for (int t = 0; t < T; t++) {
         const int64_t o = d->tree_node_offset[t];
         const int32_t *fid = d->node_fid + o;
         const float *val = d->node_value + o;
         const int32_t *lc = d->node_left + o;
         const int32_t *rcc = d->node_right + o;
-        node_base[t] = (uint32_t)np;
-        leaf_base[t] = (uint32_t)lp;
+        off16[t] = (uint32_t)(off[t] / 16);
         depth[t] = shapes[t].depth;
+        uint2 *recs = reinterpret_cast<uint2 *>(blob.data() + off[t]);
         if (layout[t] == kComplete) {
-            fill_complete(fid, val, lc, rcc, shapes[t].depth, nodes.data() + np, leaves.data() + lp);
-            np += ((int64_t)1 << shapes[t].depth) - 1;
-            lp += (int64_t)1 << shapes[t].depth;
+            const int dd = shapes[t].depth;
+            float *leaves = reinterpret_cast<float *>(blob.data() + off[t] +
+                                                      (((uint64_t)1 << dd) - 1) * 8);
+            fill_complete(fid, val, lc, rcc, dd, recs, leaves);
         } else {
-            fill_compact(fid, val, lc, rcc, shapes[t], F, nodes.data() + np);
-            np += (int64_t)shapes[t].bfs.size();
+            fill_compact(fid, val, lc, rcc, shapes[t], F, recs);
         }
     }
 
@@ -262,7 +260,7 @@ extern "C" int ts_pack(const ts_model_desc *d, int device, ts_model **out) {
             }
         }
         m->segments.push_back(Segment{layout[t], layout[t] == kComplete ? key_depth : max_depth,
-                                      t, t + 1});
+                                      t, t + 1, off[t]});
     }
     int prev = -1;
     cudaGetDevice(&prev);
@@ -271,10 +269,8 @@ extern "C" int ts_pack(const ts_model_desc *d, int device, ts_model **out) {
         delete m;
         return cuda_fail(e, "cudaSetDevice");
     }
-    int rc = upload(&m->dev.nodes, nodes);
-    if (!rc) rc = upload(&m->dev.leaves, leaves);
-    if (!rc) rc = upload(&m->dev.node_base, node_base);
-    if (!rc) rc = upload(&m->dev.leaf_base, leaf_base);
+    int rc = upload(&m->dev.blob, blob);
+    if (!rc) rc = upload(&m->dev.tree_off16, off16);
     if (!rc) rc = upload(&m->dev.depth, depth);
     if (!rc) rc = upload(&m->dev.weight, weight);
     if (prev >= 0) cudaSetDevice(prev);
@@ -290,7 +286,7 @@ extern "C" int ts_pack(const ts_model_desc *d, int device, ts_model **out) {
     info.num_segments = (int32_t)m->segments.size();
     info.sum_depth = sum_depth;
     info.table_entries = entries;
-    info.device_bytes = n_nodes * 8 + n_leaves * 4 + (int64_t)T * (4 + 4 + 4 + 8);
+    info.device_bytes = (int64_t)off[T] + (int64_t)T * (4 + 4 + 8);
     info.complete_trees = n_complete;
     info.compact_trees = n_compact;
     info.device = device;

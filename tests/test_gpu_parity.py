@@ -18,8 +18,17 @@ def _ev(model, **kw):
     return build_gpu(model, **kw)
 
 
+@pytest.fixture(params=[0, 1], ids=["auto", "l1"])
+def kernel_path(request):
+    from paper_1212_2287_b200 import _lib
+    lib = _lib.load()
+    assert lib.ts_set_kernel_path(request.param) == 0
+    yield request.param
+    lib.ts_set_kernel_path(0)
+
+
 @pytest.mark.parametrize("name", GOLDEN_CASES)
-def test_golden_scores_and_ordinals(name):
+def test_golden_scores_and_ordinals(name, kernel_path):
     ens, g = load_golden(name)
     ev = _ev(ens)
     got = ev.predict_batch(g["X"])
@@ -109,7 +118,7 @@ def test_weights_and_many_segments():
     assert np.array_equal(ev.predict_batch(g["X"]), c.score(g["X"]))
 
 
-def test_config0_full_vs_oracle():
+def test_config0_full_vs_oracle(kernel_path):
     from paper_1212_2287_b200 import synth
     w = synth.config0()
     ev = _ev(w.flat)
@@ -119,7 +128,7 @@ def test_config0_full_vs_oracle():
     assert np.array_equal(ev.leaf_indices(w.x), ref_ord.astype(np.int64))
 
 
-def test_config1_ties_subsample_vs_oracle():
+def test_config1_ties_subsample_vs_oracle(kernel_path):
     from paper_1212_2287_b200 import synth
     w = synth.config1(n=60_000)
     ev = _ev(w.flat)
@@ -130,7 +139,7 @@ def test_config1_ties_subsample_vs_oracle():
 
 
 @pytest.mark.parametrize("depth", [3, 4, 6, 8, 10, 12])
-def test_config2_depths_vs_oracle(depth):
+def test_config2_depths_vs_oracle(depth, kernel_path):
     from paper_1212_2287_b200 import synth
     w = synth.config2(depth, n=4096, trees=200)
     ev = _ev(w.flat)
