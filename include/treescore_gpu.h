@@ -135,7 +135,8 @@ int ts_synth_uniform(float *x, int64_t n, int64_t f, int64_t ld, uint64_t seed,
 
 /* Kernel-path selector for parity tests and A/B timing: 0 = automatic
  * (shared-memory streaming kernel when the tables fit, else the L1 path),
- * 1 = always the L1 (global-read) kernels.  Process-wide. */
+ * 1 = always the L1 (global-read) kernels.  Process-wide; takes effect for
+ * models packed after the call (the choice fixes the table layout). */
 int ts_set_kernel_path(int path);
 
 /* Library version string, e.g. "0.1.0 sm_100a". */

@@ -33,6 +33,8 @@ int cuda_fail(cudaError_t err, const char *what) {
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
+int kernel_path() { return g_force_l1; }
+
 void free_tables(DeviceTables *t);
 
 namespace {
@@ -63,7 +65,6 @@ int score_device(const ts_model *m, const float *x, int64_t n, int64_t f, int64_
     a.blob = m->dev.blob;
     a.tree_off16 = m->dev.tree_off16;
     a.depth = m->dev.depth;
-    a.force_l1 = g_force_l1;
     a.weight = m->dev.weight;
     a.unit_w = m->unit_weights ? 1 : 0;
     a.out = out;

@@ -25,7 +25,11 @@ namespace ts {
 //             stays put for the remaining levels of its K-group (and the
 //             predicated ordinal gains the same zero bits a dummy subtree
 //             would give it).
-enum Layout : int { kComplete = 0, kCompact = 1 };
+//  kSplit:    the streaming kernel's form of a complete tree (ts_stream.cu):
+//             heap levels < kTopLevels as {fid << kFidShift, theta} records,
+//             deeper levels as separate fp32-threshold and 1- or 2-byte fid
+//             arrays (smaller, less bank-conflicted shared-memory reads).
+enum Layout : int { kComplete = 0, kCompact = 1, kSplit = 2 };
 
 struct Segment {
     int layout;   // Layout
@@ -52,6 +56,22 @@ constexpr int kFidShift = 10;
 
 inline uint32_t complete_tree_bytes(int d) {
     return (uint32_t)((((1u << d) - 1u) * 8u + (1u << d) * 4u + 15u) & ~15u);
+}
+
+// kSplit tree record: [top records][deep thresholds][leaves][deep fids].
+constexpr int kTopLevels = 5;
+struct SplitGeom {
+    uint32_t thr0, leaf0, fid0, bytes;
+};
+inline SplitGeom split_geom(int d, int fw) {
+    const uint32_t S = d < kTopLevels ? d : kTopLevels;
+    const uint32_t deep = (1u << d) - (1u << S);
+    SplitGeom g;
+    g.thr0 = ((1u << S) - 1u) * 8u;
+    g.leaf0 = g.thr0 + deep * 4u;
+    g.fid0 = g.leaf0 + (1u << d) * 4u;
+    g.bytes = (g.fid0 + deep * (uint32_t)fw + 15u) & ~15u;
+    return g;
 }
 
 struct HostScratch {
@@ -98,12 +118,12 @@ struct ScoreArgs {
     uint16_t *ord;
     long long ld_ord;
     int32_t *status;
-    int force_l1;  // testing: use the L1-path kernels even when streaming fits
 };
 
 // Arguments of the shared-memory streaming kernel (ts_stream.cu).
 constexpr int kStreamMaxDepth = 11;
 struct StreamArgs {
+    int fw;                        // deep fid width in bytes (1: F <= 256, else 2)
     const float *x;
     long long n, ld;
     int F;
@@ -112,6 +132,7 @@ struct StreamArgs {
     uint32_t tree_bytes;           // complete_tree_bytes(D)
     int tpc;                       // trees per chunk
     uint32_t chunk_cap;            // bytes per ring stage
+    int stages;                    // ring stages (2..4)
     uint32_t xs_bytes;             // instance tile bytes
     const double *weight;
     int t0, t1;
@@ -123,6 +144,7 @@ struct StreamArgs {
     int32_t *status;
 };
 bool plan_stream(int F, int D, int device, StreamArgs *a);
+inline int split_fid_width(int F) { return F <= 256 ? 1 : 2; }
 cudaError_t launch_stream(int D, const StreamArgs &a, int device, cudaStream_t stream);
 
 // Launch the kernel of one segment; returns cudaSuccess or the launch error.
@@ -130,5 +152,6 @@ cudaError_t launch_segment(const Segment &seg, const ScoreArgs &args, int device
                            cudaStream_t stream);
 
 void count_launch();
+int kernel_path();  // ts_set_kernel_path value (0 auto, 1 L1-only)
 
 }  // namespace ts

@@ -272,9 +272,8 @@ const LaunchFn kCompleteTable[TS_MAX_DEPTH + 1] = {
 cudaError_t launch_segment(const Segment &seg, const ScoreArgs &args, int device,
                            cudaStream_t stream) {
     if (args.n <= 0) return cudaSuccess;
-    if (seg.layout == kComplete && !args.force_l1) {
+    if (seg.layout == kSplit) {
         StreamArgs sa{};
-        sa.tree_bytes = complete_tree_bytes(seg.depth);
         if (plan_stream(args.F, seg.depth, device, &sa)) {
             sa.x = args.x;
             sa.n = args.n;
@@ -293,6 +292,7 @@ cudaError_t launch_segment(const Segment &seg, const ScoreArgs &args, int device
             sa.status = args.status;
             return launch_stream(seg.depth, sa, device, stream);
         }
+        return cudaErrorInvalidConfiguration;  // packed for a device it does not fit
     }
     int optin = 0;
     cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);

@@ -92,35 +92,75 @@ int analyse_tree(const ts_model_desc *d, int t, TreeShape *s) {
     return TS_OK;
 }
 
-// Heap fill of the complete expansion (same slot algebra as the reference:
-// children of slot i at 2i+1 and 2i+2; early leaves become dummy subtrees).
-void fill_complete(const int32_t *fid, const float *val, const int32_t *lc, const int32_t *rc,
-                   int depth, uint2 *nodes, float *leaves) {
-    // Iterative level walk: src[k] = logical node occupying slot base+k.
+// Complete expansion to heap arrays (same slot algebra as the reference:
+// children of slot i at 2i+1 and 2i+2; an early leaf becomes a dummy subtree
+// of (fid 0, theta +inf) nodes whose leaves repeat its value).
+void expand_heap(const int32_t *fid, const float *val, const int32_t *lc, const int32_t *rc,
+                 int depth, std::vector<uint32_t> *hfid, std::vector<float> *hthr,
+                 std::vector<float> *hleaf) {
+    hfid->assign(((size_t)1 << depth) - 1, 0u);
+    hthr->assign(((size_t)1 << depth) - 1, INFINITY);
     std::vector<int32_t> src(1, 0), nxt;
     for (int l = 0; l < depth; l++) {
-        const uint32_t base = (1u << l) - 1u;
+        const size_t base = ((size_t)1 << l) - 1;
         nxt.resize(src.size() * 2);
         for (size_t k = 0; k < src.size(); k++) {
             int32_t i = src[k];
-            uint2 rec;
-            if (fid[i] < 0) {           // dummy: fid 0, theta +inf
-                rec.x = 0u;
-                float inf = INFINITY;
-                memcpy(&rec.y, &inf, 4);
-                nxt[2 * k] = i;
-                nxt[2 * k + 1] = i;
+            if (fid[i] < 0) {
+                nxt[2 * k] = nxt[2 * k + 1] = i;
             } else {
-                rec.x = (uint32_t)fid[i] << kFidShift;
-                memcpy(&rec.y, &val[i], 4);
+                (*hfid)[base + k] = (uint32_t)fid[i];
+                (*hthr)[base + k] = val[i];
                 nxt[2 * k] = lc[i];
                 nxt[2 * k + 1] = rc[i];
             }
-            nodes[base + k] = rec;
         }
         src.swap(nxt);
     }
-    for (size_t k = 0; k < src.size(); k++) leaves[k] = val[src[k]];
+    hleaf->resize(src.size());
+    for (size_t k = 0; k < src.size(); k++) (*hleaf)[k] = val[src[k]];
+}
+
+// kComplete: (2^d - 1) records {fid << kFidShift, theta}, then the leaves.
+void fill_complete(const int32_t *fid, const float *val, const int32_t *lc, const int32_t *rc,
+                   int depth, unsigned char *out) {
+    std::vector<uint32_t> hf;
+    std::vector<float> ht, hl;
+    expand_heap(fid, val, lc, rc, depth, &hf, &ht, &hl);
+    uint2 *recs = reinterpret_cast<uint2 *>(out);
+    for (size_t j = 0; j < hf.size(); j++) {
+        recs[j].x = hf[j] << kFidShift;
+        memcpy(&recs[j].y, &ht[j], 4);
+    }
+    memcpy(out + hf.size() * 8, hl.data(), hl.size() * 4);
+}
+
+// kSplit: see split_geom (ts_internal.h).
+void fill_split(const int32_t *fid, const float *val, const int32_t *lc, const int32_t *rc,
+                int depth, int fw, unsigned char *out) {
+    std::vector<uint32_t> hf;
+    std::vector<float> ht, hl;
+    expand_heap(fid, val, lc, rc, depth, &hf, &ht, &hl);
+    const SplitGeom g = split_geom(depth, fw);
+    const int S = depth < kTopLevels ? depth : kTopLevels;
+    uint2 *recs = reinterpret_cast<uint2 *>(out);
+    for (size_t j = 0; j + 1 < ((size_t)1 << S); j++) {
+        recs[j].x = hf[j] << kFidShift;
+        memcpy(&recs[j].y, &ht[j], 4);
+    }
+    for (int l = S; l < depth; l++) {
+        for (size_t i = 0; i < ((size_t)1 << l); i++) {
+            const size_t heap = ((size_t)1 << l) - 1 + i;
+            const size_t k = ((size_t)1 << l) - ((size_t)1 << S) + i;
+            memcpy(out + g.thr0 + 4 * k, &ht[heap], 4);
+            if (fw == 1) out[g.fid0 + k] = (unsigned char)hf[heap];
+            else {
+                const uint16_t f16 = (uint16_t)hf[heap];
+                memcpy(out + g.fid0 + 2 * k, &f16, 2);
+            }
+        }
+    }
+    memcpy(out + g.leaf0, hl.data(), hl.size() * 4);
 }
 
 // Compact BFS layout with adjacent sibling pairs and self-loop leaves.
@@ -188,6 +228,20 @@ extern "C" int ts_pack(const ts_model_desc *d, int device, ts_model **out) {
     // Compact records hold fid and the sentinel row F in 16 bits.
     const bool compact_ok_f = F <= 65534;
 
+    // Which complete depths the shared-memory streaming kernel can run on this
+    // device (instance tile + 3 ring stages fit); those trees get kSplit.
+    int prev_dev = -1;
+    cudaGetDevice(&prev_dev);
+    bool split_ok[TS_MAX_DEPTH + 1] = {};
+    if (kernel_path() == 0 && cudaSetDevice(device) == cudaSuccess) {
+        for (int dd = 0; dd <= TS_MAX_DEPTH; dd++) {
+            StreamArgs probe{};
+            split_ok[dd] = plan_stream(F, dd, device, &probe);
+        }
+    }
+    if (prev_dev >= 0) cudaSetDevice(prev_dev);
+    const int fw = split_fid_width(F);
+
     std::vector<TreeShape> shapes(T);
     std::vector<int> layout(T);
     int64_t sum_depth = 0, entries = 0;
@@ -202,7 +256,7 @@ extern "C" int ts_pack(const ts_model_desc *d, int device, ts_model **out) {
         const TreeShape &s = shapes[t];
         const int64_t nn = (int64_t)s.bfs.size();
         if (s.complete || !compact_ok_f || nn > 65535) {
-            layout[t] = kComplete;
+            layout[t] = split_ok[s.depth] ? kSplit : kComplete;
             n_complete++;
         } else {
             layout[t] = kCompact;
@@ -215,9 +269,9 @@ extern "C" int ts_pack(const ts_model_desc *d, int device, ts_model **out) {
     // Blob layout: tree t at 16 * tree_off16[t] (see DeviceTables).
     std::vector<uint64_t> off(T + 1, 0);
     for (int t = 0; t < T; t++) {
-        uint64_t bytes = layout[t] == kComplete
-                             ? complete_tree_bytes(shapes[t].depth)
-                             : ((uint64_t)shapes[t].bfs.size() * 8u + 15u) & ~(uint64_t)15u;
+        uint64_t bytes = layout[t] == kComplete ? complete_tree_bytes(shapes[t].depth)
+                         : layout[t] == kSplit ? split_geom(shapes[t].depth, fw).bytes
+                         : ((uint64_t)shapes[t].bfs.size() * 8u + 15u) & ~(uint64_t)15u;
         off[t + 1] = off[t] + bytes;
     }
     if (off[T] / 16 >= ((uint64_t)1 << 32))
@@ -234,15 +288,13 @@ extern "C" int ts_pack(const ts_model_desc *d, int device, ts_model **out) {
         const int32_t *rcc = d->node_right + o;
         off16[t] = (uint32_t)(off[t] / 16);
         depth[t] = shapes[t].depth;
-        uint2 *recs = reinterpret_cast<uint2 *>(blob.data() + off[t]);
-        if (layout[t] == kComplete) {
-            const int dd = shapes[t].depth;
-            float *leaves = reinterpret_cast<float *>(blob.data() + off[t] +
-                                                      (((uint64_t)1 << dd) - 1) * 8);
-            fill_complete(fid, val, lc, rcc, dd, recs, leaves);
-        } else {
-            fill_compact(fid, val, lc, rcc, shapes[t], F, recs);
-        }
+        unsigned char *dst = blob.data() + off[t];
+        if (layout[t] == kComplete)
+            fill_complete(fid, val, lc, rcc, shapes[t].depth, dst);
+        else if (layout[t] == kSplit)
+            fill_split(fid, val, lc, rcc, shapes[t].depth, fw, dst);
+        else
+            fill_compact(fid, val, lc, rcc, shapes[t], F, reinterpret_cast<uint2 *>(dst));
     }
 
     ts_model *m = new ts_model();
@@ -251,7 +303,7 @@ extern "C" int ts_pack(const ts_model_desc *d, int device, ts_model **out) {
     m->num_trees = T;
     m->unit_weights = unit;
     for (int t = 0; t < T; t++) {
-        int key_depth = layout[t] == kComplete ? shapes[t].depth : -1;
+        const int key_depth = layout[t] == kCompact ? -1 : shapes[t].depth;
         if (!m->segments.empty()) {
             Segment &b = m->segments.back();
             if (b.layout == layout[t] && (b.layout == kCompact || b.depth == key_depth)) {
@@ -259,7 +311,7 @@ extern "C" int ts_pack(const ts_model_desc *d, int device, ts_model **out) {
                 continue;
             }
         }
-        m->segments.push_back(Segment{layout[t], layout[t] == kComplete ? key_depth : max_depth,
+        m->segments.push_back(Segment{layout[t], layout[t] == kCompact ? max_depth : key_depth,
                                       t, t + 1, off[t]});
     }
     int prev = -1;

@@ -1,0 +1,315 @@
+#pragma once
+// ts_stream.cu -- the main sm_100a traversal kernel: complete trees whose
+// node tables are STREAMED through shared memory by the TMA bulk-copy engine.
+//
+// Per CTA (one per SM, persistent over instance tiles):
+//   * 8 consumer warps own a tile of B = 256 instances, staged from HBM and
+//     transposed to xs[f * B + r] (feature-major: lane r's x[fid] reads are
+//     bank-conflict-free for any mix of fids);
+//   * 1 producer warp streams the segment's packed trees, chunk by chunk, into
+//     an S-stage shared-memory ring with cp.async.bulk (TMA, UBLKCP in SASS);
+//     full/empty mbarriers hand stages between producer and consumers, so the
+//     next chunk (and the next tile's first chunks) land while the current
+//     one is walked;
+//   * each consumer thread walks K trees of the chunk at once (K independent
+//     index chains for latency hiding): per level
+//         rec = node[j] (LDS.64 {fid, theta});  v = xs[fid*B + r] (LDS);
+//         j = 2j + 1 + (v >= theta)
+//     -- the reference's update i = (i<<1)+1+(x[fid[i]] >= theta[i])
+//     (ref evaluators.py:90-99) -- then adds w*leaf in f64, tree order
+//     (ref evaluators.py:529-535; __dmul_rn/__dadd_rn, never an FMA).
+//
+// Chunk = `tpc` consecutive trees of one complete segment (all of depth D,
+// so every tree record has the same size and chunk c starts at
+// c * tpc * tree_bytes).  Tree record: (2^D - 1) uint2 {fid, theta bits} in
+// heap order, then 2^D fp32 leaves, padded to 16 bytes.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include <algorithm>
+
+#include "ts_internal.h"
+
+namespace ts {
+namespace stream_detail {
+
+constexpr int kConsumerWarps = 8;
+constexpr int kB = kConsumerWarps * 32;  // instances per tile
+constexpr int kThreads = kB + 32;        // + producer warp
+constexpr int kMaxStages = 4;
+
+// Chains per thread by depth: deeper trees are bigger, so fewer fit in a
+// ring stage (a K-group must fit one stage).
+__host__ __device__ constexpr int chains_for_depth(int d) { return d <= 9 ? 8 : d == 10 ? 4 : 2; }
+
+__device__ __forceinline__ uint32_t su32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(su32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes,
+                                         uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(su32(dst)),
+        "l"(src), "r"(bytes), "r"(su32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void consumer_sync() {
+    asm volatile("bar.sync 1, %0;" ::"n"(kB) : "memory");
+}
+__device__ __forceinline__ bool finite_f(float v) { return fabsf(v) <= 3.402823466e38f; }
+
+// Transposing stage of B rows into xs[f * kB + r] (consumer threads only).
+__device__ __forceinline__ void stage_rows(const StreamArgs &a, float *xs, long long row0) {
+    const int r = threadIdx.x;
+    const long long row = row0 + r;
+    const bool valid = row < a.n;
+    const float *xrow = a.x + (valid ? row : 0) * a.ld;
+    const int F = a.F;
+    bool bad = false;
+    if (((F & 3) == 0) && ((a.ld & 3) == 0) && ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0)) {
+        const float4 *x4 = reinterpret_cast<const float4 *>(xrow);
+        int c = 0;
+        for (; c + 16 <= F; c += 16) {
+            float4 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++)
+                v[u] = valid ? __ldg(x4 + (c >> 2) + u) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                bad |= !(finite_f(v[u].x) && finite_f(v[u].y) && finite_f(v[u].z) &&
+                         finite_f(v[u].w));
+                float *dst = xs + (c + 4 * u) * kB + r;
+                dst[0] = v[u].x;
+                dst[kB] = v[u].y;
+                dst[2 * kB] = v[u].z;
+                dst[3 * kB] = v[u].w;
+            }
+        }
+        for (; c < F; c += 4) {
+            float4 v = valid ? __ldg(x4 + (c >> 2)) : make_float4(0.f, 0.f, 0.f, 0.f);
+            bad |= !(finite_f(v.x) && finite_f(v.y) && finite_f(v.z) && finite_f(v.w));
+            float *dst = xs + c * kB + r;
+            dst[0] = v.x;
+            dst[kB] = v.y;
+            dst[2 * kB] = v.z;
+            dst[3 * kB] = v.w;
+        }
+    } else {
+        for (int c = 0; c < F; c++) {
+            float v = valid ? __ldg(xrow + c) : 0.f;
+            bad |= !finite_f(v);
+            xs[c * kB + r] = v;
+        }
+    }
+    if (bad && a.status) atomicOr(a.status, 1);
+}
+
+__device__ __forceinline__ uint2 lds64(uint32_t addr) {
+    uint2 v;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ float ldsf(uint32_t addr) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+    return v;
+}
+
+__device__ __forceinline__ uint32_t ldsu(uint32_t addr, int fw) {
+    uint32_t v;
+    if (fw == 1) asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
+    else asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+
+// Walk NK trees of one chunk in lockstep (NK independent chains) over the
+// kSplit record (ts_internal.h):
+//  * top levels (< kTopLevels): records {fid << 10, theta}; the chain state is
+//    the record's shared address p and the heap step j -> 2j + 1 + c becomes
+//    p -> 2p + (c ? 16 - base : 8 - base);
+//  * deep levels: per-level arrays thr[2^l] (fp32) and fid[2^l] (FW bytes);
+//    state v = base_fid + FW * i (i = index within the level), the step
+//    i -> 2i + c becomes v -> 2v - base_fid + FW * c and the threshold sits at
+//    (4/FW) * v + kq + per-level immediate.
+template <int D, int NK, int FW, bool UNIT_W, bool ORD>
+__device__ __forceinline__ void walk_group(uint32_t tree0, uint32_t tree_bytes, uint32_t xr,
+                                           double &acc, const StreamArgs &a, int t,
+                                           long long row, bool valid) {
+    constexpr int S = D < kTopLevels ? D : kTopLevels;
+    constexpr uint32_t kThr0 = ((1u << S) - 1u) * 8u;
+    constexpr uint32_t kDeep = (1u << D) - (1u << S);
+    constexpr uint32_t kLeaf0 = kThr0 + kDeep * 4u;
+    constexpr uint32_t kFid0 = kLeaf0 + (1u << D) * 4u;
+    constexpr int kShift = FW == 1 ? 2 : 1;  // thr address = v << kShift + kq
+    uint32_t p[NK];
+#pragma unroll
+    for (int k = 0; k < NK; k++) p[k] = tree0 + k * tree_bytes;
+#pragma unroll
+    for (int l = 0; l < S; l++) {
+#pragma unroll
+        for (int k = 0; k < NK; k++) {
+            const uint32_t base = tree0 + k * tree_bytes;
+            const uint2 q = lds64(p[k]);
+            const float v = ldsf(q.x + xr);
+            p[k] = 2u * p[k] + (v >= __uint_as_float(q.y) ? 16u - base : 8u - base);
+        }
+    }
+    uint32_t idx[NK];  // D <= S: heap index of the leaf; D > S: v state
+    if constexpr (D > S) {
+#pragma unroll
+        for (int k = 0; k < NK; k++) {
+            const uint32_t base = tree0 + k * tree_bytes;
+            const uint32_t bf = base + kFid0;
+            // leaving the top: heap slot j = (p - base) / 8, index in level S
+            idx[k] = bf + FW * (((p[k] - base) >> 3) - ((1u << S) - 1u));
+        }
+#pragma unroll
+        for (int l = S; l < D; l++) {
+            const uint32_t lvl = (1u << l) - (1u << S);
+#pragma unroll
+            for (int k = 0; k < NK; k++) {
+                const uint32_t base = tree0 + k * tree_bytes;
+                const uint32_t bf = base + kFid0;
+                const uint32_t kq = base + kThr0 - (bf << kShift);
+                const float th = ldsf((idx[k] << kShift) + kq + 4u * lvl);
+                const uint32_t fid = ldsu(idx[k] + FW * lvl, FW);
+                const float v = ldsf(fid * (kB * 4u) + xr);
+                idx[k] = 2u * idx[k] + (v >= th ? (uint32_t)FW - bf : 0u - bf);
+            }
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < NK; k++) {
+        const uint32_t base = tree0 + k * tree_bytes;
+        uint32_t ord;
+        if constexpr (D > S) {
+            ord = (idx[k] - (base + kFid0)) / FW;
+        } else {
+            ord = ((p[k] - base) >> 3) - ((1u << D) - 1u);
+        }
+        const float lv = ldsf(base + kLeaf0 + ord * 4u);
+        if constexpr (UNIT_W) acc = __dadd_rn(acc, (double)lv);
+        else acc = __dadd_rn(acc, __dmul_rn(__ldg(a.weight + t + k), (double)lv));
+        if constexpr (ORD) {
+            if (valid) a.ord[(long long)(t + k) * a.ld_ord + row] = (uint16_t)ord;
+        }
+    }
+}
+
+template <int D, int K, int FW, bool UNIT_W, bool ORD>
+__global__ void __launch_bounds__(kThreads, 1) k_stream(StreamArgs a) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    float *xs = reinterpret_cast<float *>(smem);
+    unsigned char *ring = smem + a.xs_bytes;
+    const int kStages = a.stages;
+    uint64_t *full = reinterpret_cast<uint64_t *>(ring + kStages * a.chunk_cap);
+    uint64_t *empty = full + kMaxStages;
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kMaxStages; s++) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, kConsumerWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const long long ntiles = (a.n + kB - 1) / kB;
+    const int nchunks = (a.t1 - a.t0 + a.tpc - 1) / a.tpc;
+
+    if (warp == kConsumerWarps) {  // ---- producer warp: TMA bulk copies
+        if (lane == 0) {
+            uint32_t it = 0;
+            for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                for (int c = 0; c < nchunks; c++, it++) {
+                    const int s = it % kStages;
+                    if (it >= kStages) mbar_wait(empty + s, ((it / kStages) - 1) & 1);
+                    const int trees = min(a.tpc, a.t1 - a.t0 - c * a.tpc);
+                    const uint32_t bytes = (uint32_t)trees * a.tree_bytes;
+                    mbar_expect_tx(full + s, bytes);
+                    bulk_g2s(ring + s * a.chunk_cap,
+                             a.blob + a.seg_byte0 + (size_t)c * a.tpc * a.tree_bytes, bytes,
+                             full + s);
+                }
+            }
+        }
+        return;
+    }
+
+    // ---- consumer warps
+    const int r = threadIdx.x;
+    const uint32_t xr = su32(xs) + 4u * r;
+    uint32_t it = 0;
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const long long row = tile * kB + r;
+        const bool valid = row < a.n;
+        consumer_sync();  // previous tile's walks are done with xs
+        stage_rows(a, xs, tile * kB);
+        consumer_sync();
+        double acc = (a.accumulate && valid) ? a.out[row] : 0.0;
+        for (int c = 0; c < nchunks; c++, it++) {
+            const int s = it % kStages;
+            mbar_wait(full + s, (it / kStages) & 1);
+            const uint32_t buf = su32(ring + s * a.chunk_cap);
+            const int t0 = a.t0 + c * a.tpc;
+            const int trees = min(a.tpc, a.t1 - t0);
+            int k = 0;
+            for (; k + K <= trees; k += K)
+                walk_group<D, K, FW, UNIT_W, ORD>(buf + k * a.tree_bytes, a.tree_bytes, xr, acc,
+                                                  a, t0 + k, row, valid);
+            for (; k < trees; k++)
+                walk_group<D, 1, FW, UNIT_W, ORD>(buf + k * a.tree_bytes, a.tree_bytes, xr, acc,
+                                                  a, t0 + k, row, valid);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty + s);
+        }
+        if (valid) a.out[row] = acc;
+    }
+}
+
+template <int D, int FW>
+auto pick_kernel(const StreamArgs &a) {
+    constexpr int K = chains_for_depth(D);
+    if (a.ord) return a.unit_w ? k_stream<D, K, FW, true, true> : k_stream<D, K, FW, false, true>;
+    return a.unit_w ? k_stream<D, K, FW, true, false> : k_stream<D, K, FW, false, false>;
+}
+
+template <int D>
+cudaError_t launch_d(const StreamArgs &a, int device, cudaStream_t stream) {
+    auto kern = a.fw == 1 ? pick_kernel<D, 1>(a) : pick_kernel<D, 2>(a);
+    int sms = 0;
+    cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    if (e != cudaSuccess) return e;
+    const size_t smem = a.xs_bytes + (size_t)a.stages * a.chunk_cap + 2 * kMaxStages * 8;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const long long tiles = (a.n + kB - 1) / kB;
+    const int grid = (int)(tiles < sms ? tiles : sms);
+    kern<<<grid, kThreads, smem, stream>>>(a);
+    count_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace stream_detail
+}  // namespace ts

@@ -1,0 +1,122 @@
+"""Time every BASELINE configuration on one GPU and check parity on a sample.
+
+    python tools/bench_configs.py [--configs 0,1,2:3,...] [--reps 5] [--out FILE]
+
+Config keys: 0, 1, 2:<d> (d in 3,4,6,8,10,12), 3, 4a, 4b.  Instances are
+device-resident (configs 3/4 generated in place on the GPU by the
+counter-based generator, bit-identical to the host reproduction used for the
+oracle sample).  One JSON line per config: tree-evals/s (CUDA events, mean of
+--reps launches after warm-up), the SURVEY section 8(d) roofline fraction
+(slower of HBM feature bytes and 4-issue-slot node visits at sm_max_mhz), and
+a bit-exact parity check of a row sample against the C oracle.
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import oracle  # noqa: E402
+from paper_1212_2287_b200 import _lib, build_gpu, synth  # noqa: E402
+
+
+def peaks():
+    try:
+        p = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(p["hbm_gbs"]), float(p["sm_max_mhz"])
+    except Exception:  # noqa: BLE001
+        return 6650.0, 1965.0
+
+
+def workload(key):
+    if key == "0":
+        return synth.config0()
+    if key == "1":
+        return synth.config1()
+    if key.startswith("2:"):
+        return synth.config2(int(key[2:]))
+    if key == "3":
+        return synth.config3()
+    if key == "4a":
+        return synth.config4a()
+    if key == "4b":
+        return synth.config4b()
+    raise ValueError(key)
+
+
+def device_rows(w, dev):
+    if w.x is not None:
+        return torch.from_numpy(w.x).to(dev)
+    x = torch.empty((w.n, w.f), dtype=torch.float32, device=dev)
+    rc = _lib.load().ts_synth_uniform(x.data_ptr(), w.n, w.f, w.f, w.hash_seed, 0, w.zero_prob,
+                                      torch.cuda.current_stream(dev).cuda_stream)
+    assert rc == 0, _lib.last_error()
+    return x
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="0,1,2:3,2:4,2:6,2:8,2:10,2:12,3,4a,4b")
+    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--sample", type=int, default=4096)
+    ap.add_argument("--out", default=None)
+    a = ap.parse_args()
+    dev = torch.device("cuda", 0)
+    hbm, fmhz = peaks()
+    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+    visit_peak = n_sm * 128 * fmhz * 1e6 / 4
+    lines = []
+    for key in a.configs.split(","):
+        t0 = time.time()
+        w = workload(key)
+        gen_s = time.time() - t0
+        ev = build_gpu(w.flat, device=0)
+        info = ev.model.info
+        x = device_rows(w, dev)
+        out = torch.empty(w.n, dtype=torch.float64, device=dev)
+        ev.score_device(x, out=out)
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(a.reps):
+            ev.score_device(x, out=out)
+        e.record()
+        torch.cuda.synchronize()
+        ms = s.elapsed_time(e) / a.reps
+        T = w.flat.num_trees
+        evals = w.n * T / (ms / 1e3)
+        t_hbm = w.n * (4 * w.f + 8) / (hbm * 1e9)
+        t_issue = w.n * info["sum_depth"] / visit_peak
+        roof = w.n * T / max(t_hbm, t_issue)
+        # parity: a row sample (spread over the matrix) against the C oracle
+        rows = np.unique(np.linspace(0, w.n - 1, min(a.sample, w.n)).astype(np.int64))
+        got = out.cpu().numpy()[rows]
+        host = np.concatenate([w.rows(int(r), 1) for r in rows]) if w.x is None \
+            else w.x[rows]
+        ref = oracle.COracle(w.flat.arrays()).score(host)
+        line = {"config": key, "workload": w.name, "n": w.n, "f": w.f, "trees": T,
+                "sum_depth": info["sum_depth"], "segments": info["num_segments"],
+                "complete_trees": info["complete_trees"], "compact_trees": info["compact_trees"],
+                "ms_per_pass": ms, "tree_evals_per_s": evals,
+                "roofline_bound": "issue" if t_issue > t_hbm else "hbm",
+                "roofline_evals_per_s": roof, "roofline_frac": evals / roof,
+                "parity_rows": int(len(rows)), "bit_exact": bool(np.array_equal(got, ref)),
+                "max_abs_err": float(np.max(np.abs(got - ref))), "gen_s": gen_s}
+        print(json.dumps(line), flush=True)
+        lines.append(line)
+        del x, out, ev
+        torch.cuda.empty_cache()
+    if a.out:
+        with open(a.out, "w") as fh:
+            for line in lines:
+                fh.write(json.dumps(line) + "\n")
+
+
+if __name__ == "__main__":
+    main()
