@@ -62,6 +62,7 @@ int score_device(const ts_model *m, const float *x, int64_t n, int64_t f, int64_
     a.n = n;
     a.ld = ld;
     a.F = m->num_features;
+    a.tables = &m->dev;
     a.blob = m->dev.blob;
     a.tree_off16 = m->dev.tree_off16;
     a.depth = m->dev.depth;

@@ -29,13 +29,17 @@ namespace ts {
 //             heap levels < kTopLevels as {fid << kFidShift, theta} records,
 //             deeper levels as separate fp32-threshold and 1- or 2-byte fid
 //             arrays (smaller, less bank-conflicted shared-memory reads).
-enum Layout : int { kComplete = 0, kCompact = 1, kSplit = 2 };
+//  kCStream:  kCompact for the irregular-tree streaming kernel (ts_cstream.cu):
+//             record {fid | (8 * left) << 16, theta}; leaf {F | (8 * self) << 16,
+//             value}; trees of <= 8191 nodes, grouped into chunks.
+enum Layout : int { kComplete = 0, kCompact = 1, kSplit = 2, kCStream = 3 };
 
 struct Segment {
     int layout;   // Layout
     int depth;    // kComplete: the common depth of every tree in the segment
     int t0, t1;   // tree range [t0, t1) in evaluation order
     uint64_t byte0;  // blob offset of tree t0
+    int chunk0 = 0, nchunks = 0;  // kCStream: chunk table range
 };
 
 // All trees live in one byte blob, tree t at byte 16 * tree_off16[t]:
@@ -48,6 +52,10 @@ struct DeviceTables {
     uint32_t *tree_off16 = nullptr;  // [T]
     int32_t *depth = nullptr;        // [T]
     double *weight = nullptr;        // [T]
+    // kCStream chunk tables
+    uint4 *chunk_info = nullptr;     // {blob off / 16, bytes, trees, first tree}
+    uint32_t *slot_meta = nullptr;   // [chunks][kCStreamMaxT] rec_off/8 | depth<<16 | rel<<21
+    unsigned char *slot_inv = nullptr;  // [chunks][kCStreamMaxT] tree rel -> slot
 };
 
 // kComplete records store fid << kFidShift: the byte offset of feature fid's
@@ -107,6 +115,7 @@ struct ScoreArgs {
     const float *x;
     long long n, ld;
     int F;
+    const DeviceTables *tables;
     const unsigned char *blob;
     const uint32_t *tree_off16;
     const int32_t *depth;
@@ -146,6 +155,31 @@ struct StreamArgs {
 bool plan_stream(int F, int D, int device, StreamArgs *a);
 inline int split_fid_width(int F) { return F <= 256 ? 1 : 2; }
 cudaError_t launch_stream(int D, const StreamArgs &a, int device, cudaStream_t stream);
+
+// Irregular-tree streaming kernel (ts_cstream.cu).
+constexpr int kCStreamMaxT = 32;     // tree slots per chunk
+constexpr int kCStreamMaxNodes = 8191;
+struct CStreamArgs {
+    const float *x;
+    long long n, ld;
+    int F;
+    int B;                 // instances per tile (32 * G)
+    const unsigned char *blob;
+    const uint4 *chunk_info;
+    const uint32_t *slot_meta;
+    const unsigned char *slot_inv;
+    int chunk0, nchunks;
+    int tpc;               // max trees per chunk
+    uint32_t chunk_cap, xs_bytes, lb_bytes;
+    const double *weight;
+    int unit_w, accumulate;
+    double *out;
+    uint16_t *ord;
+    long long ld_ord;
+    int32_t *status;
+};
+bool plan_cstream(int F, int device, CStreamArgs *a);
+cudaError_t launch_cstream(const CStreamArgs &a, int device, cudaStream_t stream);
 
 // Launch the kernel of one segment; returns cudaSuccess or the launch error.
 cudaError_t launch_segment(const Segment &seg, const ScoreArgs &args, int device,

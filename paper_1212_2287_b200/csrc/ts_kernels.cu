@@ -272,6 +272,28 @@ const LaunchFn kCompleteTable[TS_MAX_DEPTH + 1] = {
 cudaError_t launch_segment(const Segment &seg, const ScoreArgs &args, int device,
                            cudaStream_t stream) {
     if (args.n <= 0) return cudaSuccess;
+    if (seg.layout == kCStream) {
+        CStreamArgs ca{};
+        if (!plan_cstream(args.F, device, &ca)) return cudaErrorInvalidConfiguration;
+        ca.x = args.x;
+        ca.n = args.n;
+        ca.ld = args.ld;
+        ca.F = args.F;
+        ca.blob = args.blob;
+        ca.chunk_info = args.tables->chunk_info;
+        ca.slot_meta = args.tables->slot_meta;
+        ca.slot_inv = args.tables->slot_inv;
+        ca.chunk0 = seg.chunk0;
+        ca.nchunks = seg.nchunks;
+        ca.weight = args.weight;
+        ca.unit_w = args.unit_w;
+        ca.accumulate = args.accumulate;
+        ca.out = args.out;
+        ca.ord = args.ord;
+        ca.ld_ord = args.ld_ord;
+        ca.status = args.status;
+        return launch_cstream(ca, device, stream);
+    }
     if (seg.layout == kSplit) {
         StreamArgs sa{};
         if (plan_stream(args.F, seg.depth, device, &sa)) {

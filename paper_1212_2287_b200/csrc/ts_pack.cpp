@@ -164,8 +164,9 @@ void fill_split(const int32_t *fid, const float *val, const int32_t *lc, const i
 }
 
 // Compact BFS layout with adjacent sibling pairs and self-loop leaves.
+// child_scale 1: kCompact (child index << 16); 8: kCStream (child byte offset).
 void fill_compact(const int32_t *fid, const float *val, const int32_t *lc, const int32_t *rc,
-                  const TreeShape &s, int F, uint2 *nodes) {
+                  const TreeShape &s, int F, uint2 *nodes, uint32_t child_scale) {
     const int32_t n = (int32_t)s.bfs.size();
     std::vector<int32_t> newid(n, -1);
     std::vector<int32_t> order;
@@ -184,8 +185,8 @@ void fill_compact(const int32_t *fid, const float *val, const int32_t *lc, const
         int32_t i = order[k];
         uint2 rec;
         memcpy(&rec.y, &val[i], 4);
-        if (fid[i] < 0) rec.x = (uint32_t)F | ((uint32_t)k << 16);
-        else rec.x = (uint32_t)fid[i] | ((uint32_t)newid[lc[i]] << 16);
+        if (fid[i] < 0) rec.x = (uint32_t)F | ((uint32_t)k * child_scale << 16);
+        else rec.x = (uint32_t)fid[i] | ((uint32_t)newid[lc[i]] * child_scale << 16);
         nodes[k] = rec;
     }
 }
@@ -209,6 +210,9 @@ void free_tables(DeviceTables *t) {
     cudaFree(t->tree_off16);
     cudaFree(t->depth);
     cudaFree(t->weight);
+    cudaFree(t->chunk_info);
+    cudaFree(t->slot_meta);
+    cudaFree(t->slot_inv);
     *t = DeviceTables{};
 }
 
@@ -239,6 +243,10 @@ extern "C" int ts_pack(const ts_model_desc *d, int device, ts_model **out) {
             split_ok[dd] = plan_stream(F, dd, device, &probe);
         }
     }
+    CStreamArgs cplan{};
+    const bool cstream_ok = kernel_path() == 0 && compact_ok_f &&
+                            cudaSetDevice(device) == cudaSuccess &&
+                            plan_cstream(F, device, &cplan);
     if (prev_dev >= 0) cudaSetDevice(prev_dev);
     const int fw = split_fid_width(F);
 
@@ -259,7 +267,9 @@ extern "C" int ts_pack(const ts_model_desc *d, int device, ts_model **out) {
             layout[t] = split_ok[s.depth] ? kSplit : kComplete;
             n_complete++;
         } else {
-            layout[t] = kCompact;
+            const uint64_t tb = ((uint64_t)nn * 8u + 15u) & ~(uint64_t)15u;
+            layout[t] = (cstream_ok && nn <= kCStreamMaxNodes && tb <= cplan.chunk_cap)
+                            ? kCStream : kCompact;
             n_compact++;
         }
         sum_depth += s.depth;
@@ -294,7 +304,8 @@ extern "C" int ts_pack(const ts_model_desc *d, int device, ts_model **out) {
         else if (layout[t] == kSplit)
             fill_split(fid, val, lc, rcc, shapes[t].depth, fw, dst);
         else
-            fill_compact(fid, val, lc, rcc, shapes[t], F, reinterpret_cast<uint2 *>(dst));
+            fill_compact(fid, val, lc, rcc, shapes[t], F, reinterpret_cast<uint2 *>(dst),
+                         layout[t] == kCStream ? 8u : 1u);
     }
 
     ts_model *m = new ts_model();
@@ -303,16 +314,52 @@ extern "C" int ts_pack(const ts_model_desc *d, int device, ts_model **out) {
     m->num_trees = T;
     m->unit_weights = unit;
     for (int t = 0; t < T; t++) {
-        const int key_depth = layout[t] == kCompact ? -1 : shapes[t].depth;
+        const bool any_depth = layout[t] == kCompact || layout[t] == kCStream;
+        const int key_depth = any_depth ? -1 : shapes[t].depth;
         if (!m->segments.empty()) {
             Segment &b = m->segments.back();
-            if (b.layout == layout[t] && (b.layout == kCompact || b.depth == key_depth)) {
+            if (b.layout == layout[t] && (any_depth || b.depth == key_depth)) {
                 b.t1 = t + 1;
                 continue;
             }
         }
-        m->segments.push_back(Segment{layout[t], layout[t] == kCompact ? max_depth : key_depth,
-                                      t, t + 1, off[t]});
+        m->segments.push_back(Segment{layout[t], any_depth ? max_depth : key_depth, t, t + 1,
+                                      off[t]});
+    }
+    // kCStream chunk tables: consecutive trees up to tpc / chunk_cap bytes;
+    // inside a chunk the slots are ordered by depth (deepest first) so the
+    // kernel's lockstep K-groups walk trees of nearly equal depth.
+    std::vector<uint4> chunk_info;
+    std::vector<uint32_t> slot_meta;
+    std::vector<unsigned char> slot_inv;
+    for (Segment &sg : m->segments) {
+        if (sg.layout != kCStream) continue;
+        sg.chunk0 = (int)chunk_info.size();
+        int t = sg.t0;
+        while (t < sg.t1) {
+            int e = t;
+            while (e < sg.t1 && e - t < cplan.tpc && off[e + 1] - off[t] <= cplan.chunk_cap) e++;
+            const int nt = e - t;
+            chunk_info.push_back(make_uint4((uint32_t)(off[t] / 16), (uint32_t)(off[e] - off[t]),
+                                            (uint32_t)nt, (uint32_t)t));
+            std::vector<int> order(nt);
+            for (int i = 0; i < nt; i++) order[i] = i;
+            std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
+                return shapes[t + x].depth > shapes[t + y].depth;
+            });
+            const size_t base = slot_meta.size();
+            slot_meta.resize(base + kCStreamMaxT, 0u);
+            slot_inv.resize(base + kCStreamMaxT, 0);
+            for (int sl = 0; sl < nt; sl++) {
+                const int rel = order[sl];
+                const uint32_t rec8 = (uint32_t)((off[t + rel] - off[t]) / 8);
+                slot_meta[base + sl] = rec8 | ((uint32_t)shapes[t + rel].depth << 16) |
+                                       ((uint32_t)rel << 21);
+                slot_inv[base + rel] = (unsigned char)sl;
+            }
+            t = e;
+        }
+        sg.nchunks = (int)chunk_info.size() - sg.chunk0;
     }
     int prev = -1;
     cudaGetDevice(&prev);
@@ -325,6 +372,9 @@ extern "C" int ts_pack(const ts_model_desc *d, int device, ts_model **out) {
     if (!rc) rc = upload(&m->dev.tree_off16, off16);
     if (!rc) rc = upload(&m->dev.depth, depth);
     if (!rc) rc = upload(&m->dev.weight, weight);
+    if (!rc) rc = upload(&m->dev.chunk_info, chunk_info);
+    if (!rc) rc = upload(&m->dev.slot_meta, slot_meta);
+    if (!rc) rc = upload(&m->dev.slot_inv, slot_inv);
     if (prev >= 0) cudaSetDevice(prev);
     if (rc) {
         free_tables(&m->dev);
