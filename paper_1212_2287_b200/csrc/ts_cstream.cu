@@ -13,7 +13,8 @@
 //    thread walks in lockstep have nearly equal depth (a K-group steps
 //    max(depth) times; a leaf is a self-loop whose x row is the -inf sentinel
 //    row F, so shorter trees idle on their leaf);
-//  * each walk writes its leaf value to a shared leaf buffer lb[slot][inst];
+//  * each walk writes its leaf value to a shared leaf buffer lb[tree][inst]
+//    (tree = the slot's position in evaluation order within the chunk);
 //    after the chunk, thread `inst` folds the chunk's leaves into its f64
 //    accumulator in TREE order (acc = acc + w * leaf, __dmul_rn/__dadd_rn),
 //    so the result stays bit-identical to the reference's sequential sum
@@ -25,6 +26,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "ts_internal.h"
 #include "ts_stream_kernel.cuh"
@@ -37,8 +39,8 @@ using namespace stream_detail;
 constexpr int kWarps = 8;
 constexpr int kConsumers = kWarps * 32;
 constexpr int kThreadsC = kConsumers + 32;
-constexpr int kK = 4;  // lockstep chains per thread
 constexpr int kStagesC = 2;
+constexpr uint32_t kMetaBytes = kCStreamMaxT * 4;  // slot table at the head of a stage
 
 // Stage B rows x F features into xs[f * B + r] (+ sentinel row F = -inf),
 // all 256 consumer threads cooperating.
@@ -51,17 +53,31 @@ __device__ __forceinline__ void stage_rows_c(const CStreamArgs &a, float *xs, lo
                      ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0);
     if (vec) {
         const int F4 = F >> 2;
-        for (int e = tid; e < B * F4; e += kConsumers) {
-            const int r = e % B, c4 = e / B;
-            const long long row = row0 + r;
-            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (row < a.n) v = __ldg(reinterpret_cast<const float4 *>(a.x + row * a.ld) + c4);
-            bad |= !(finite_f(v.x) && finite_f(v.y) && finite_f(v.z) && finite_f(v.w));
-            float *dst = xs + (4 * c4) * B + r;
-            dst[0] = v.x;
-            dst[B] = v.y;
-            dst[2 * B] = v.z;
-            dst[3 * B] = v.w;
+        constexpr int U = 8;  // independent loads in flight per thread
+        for (int e0 = tid; e0 < B * F4; e0 += U * kConsumers) {
+            float4 v[U];
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const int e = e0 + u * kConsumers;
+                const int r = e % B, c4 = e / B;
+                const long long row = row0 + r;
+                v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (e < B * F4 && row < a.n)
+                    v[u] = __ldg(reinterpret_cast<const float4 *>(a.x + row * a.ld) + c4);
+            }
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const int e = e0 + u * kConsumers;
+                if (e >= B * F4) break;
+                const int r = e % B, c4 = e / B;
+                bad |= !(finite_f(v[u].x) && finite_f(v[u].y) && finite_f(v[u].z) &&
+                         finite_f(v[u].w));
+                float *dst = xs + (4 * c4) * B + r;
+                dst[0] = v[u].x;
+                dst[B] = v[u].y;
+                dst[2 * B] = v[u].z;
+                dst[3 * B] = v[u].w;
+            }
         }
     } else {
         for (int e = tid; e < B * F; e += kConsumers) {
@@ -76,13 +92,13 @@ __device__ __forceinline__ void stage_rows_c(const CStreamArgs &a, float *xs, lo
     if (bad && a.status) atomicOr(a.status, 1);
 }
 
-template <bool UNIT_W, bool ORD>
+template <int kK, bool UNIT_W, bool ORD>
 __global__ void __launch_bounds__(kThreadsC, 1) k_cstream(CStreamArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     float *xs = reinterpret_cast<float *>(smem);
-    float *lb = reinterpret_cast<float *>(smem + a.xs_bytes);
+    float *lb0 = reinterpret_cast<float *>(smem + a.xs_bytes);  // two leaf buffers
     unsigned char *ring = smem + a.xs_bytes + a.lb_bytes;
-    uint64_t *full = reinterpret_cast<uint64_t *>(ring + kStagesC * a.chunk_cap);
+    uint64_t *full = reinterpret_cast<uint64_t *>(ring + kStagesC * a.stage_bytes);
     uint64_t *empty = full + kStagesC;
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -105,8 +121,11 @@ __global__ void __launch_bounds__(kThreadsC, 1) k_cstream(CStreamArgs a) {
                     const int s = it % kStagesC;
                     if (it >= kStagesC) mbar_wait(empty + s, ((it / kStagesC) - 1) & 1);
                     const uint4 ci = __ldg(a.chunk_info + a.chunk0 + c);
-                    mbar_expect_tx(full + s, ci.y);
-                    bulk_g2s(ring + s * a.chunk_cap, a.blob + 16ull * ci.x, ci.y, full + s);
+                    unsigned char *stage = ring + s * a.stage_bytes;
+                    mbar_expect_tx(full + s, ci.y + kMetaBytes);
+                    bulk_g2s(stage, a.slot_meta + (size_t)(a.chunk0 + c) * kCStreamMaxT,
+                             kMetaBytes, full + s);
+                    bulk_g2s(stage + kMetaBytes, a.blob + 16ull * ci.x, ci.y, full + s);
                 }
             }
         }
@@ -122,7 +141,8 @@ __global__ void __launch_bounds__(kThreadsC, 1) k_cstream(CStreamArgs a) {
     const int inst = grp * 32 + lane;
     const uint32_t xr = su32(xs) + 4u * inst;
     const uint32_t B4 = 4u * B;
-    const uint32_t lbase = su32(lb);
+    const uint32_t lbase0 = su32(lb0);
+    const uint32_t lb_half = a.lb_bytes / 2;
     uint32_t it = 0;
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const long long row0 = tile * B;
@@ -137,17 +157,21 @@ __global__ void __launch_bounds__(kThreadsC, 1) k_cstream(CStreamArgs a) {
             const int s = it % kStagesC;
             const uint4 ci = __ldg(a.chunk_info + a.chunk0 + c);
             const int nt = (int)ci.z;
-            const uint32_t *meta = a.slot_meta + (size_t)(a.chunk0 + c) * kCStreamMaxT;
+            const uint32_t lbase = lbase0 + (it & 1) * lb_half;
             mbar_wait(full + s, (it / kStagesC) & 1);
-            const uint32_t buf = su32(ring + s * a.chunk_cap);
+            const uint32_t meta = su32(ring + s * a.stage_bytes);
+            const uint32_t buf = meta + kMetaBytes;
             for (int s0 = sub; s0 < nt; s0 += S * kK) {
-                uint32_t p[kK], tb[kK], ob[kK];
+                uint32_t p[kK], tb[kK], ob[kK], rel[kK];
                 int dk[kK];
                 int dmax = 0;
 #pragma unroll
                 for (int k = 0; k < kK; k++) {
                     const int slot = s0 + k * S;
-                    const uint32_t m = slot < nt ? __ldg(meta + slot) : __ldg(meta + s0);
+                    uint32_t m;
+                    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(m)
+                                 : "r"(meta + 4u * (slot < nt ? slot : s0)));
+                    rel[k] = m >> 21;
                     tb[k] = buf + 8u * (m & 0xffffu);
                     p[k] = tb[k];
                     dk[k] = (m >> 16) & 31;
@@ -170,29 +194,42 @@ __global__ void __launch_bounds__(kThreadsC, 1) k_cstream(CStreamArgs a) {
                     const int slot = s0 + k * S;
                     if (slot < nt) {
                         const float lv = ldsf(p[k] + 4u);
-                        asm volatile("st.shared.f32 [%0], %1;" ::"r"(lbase + 4u * (slot * B + inst)),
+                        asm volatile("st.shared.f32 [%0], %1;" ::"r"(lbase + 4u * (rel[k] * B + inst)),
                                      "f"(lv));
                         if constexpr (ORD) {
-                            if (walk_valid) {
-                                const uint32_t rel = __ldg(meta + slot) >> 21;
-                                a.ord[(long long)(ci.w + rel) * a.ld_ord + walk_row] =
+                            if (walk_valid)
+                                a.ord[(long long)(ci.w + rel[k]) * a.ld_ord + walk_row] =
                                     (uint16_t)(ob[k] >> (dmax - dk[k]));
-                            }
                         }
                     }
                 }
             }
-            consumer_sync();  // leaf buffer complete; ring stage fully read
+            // One barrier per chunk: it publishes this chunk's leaf buffer and
+            // frees its ring stage.  The other leaf buffer (written by the
+            // next chunk) was last read before this barrier, so no second one.
+            consumer_sync();
             if (tid == 0) mbar_arrive(empty + s);
             if (tid < B) {
-                const unsigned char *inv = a.slot_inv + (size_t)(a.chunk0 + c) * kCStreamMaxT;
-                for (int i = 0; i < nt; i++) {
-                    const float lv = lb[__ldg(inv + i) * B + tid];
+                const float *lbc = reinterpret_cast<const float *>(
+                    reinterpret_cast<const unsigned char *>(lb0) + (it & 1) * lb_half);
+                int i = 0;
+                for (; i + 8 <= nt; i += 8) {
+                    float lv[8];
+#pragma unroll
+                    for (int u = 0; u < 8; u++) lv[u] = lbc[(i + u) * B + tid];
+#pragma unroll
+                    for (int u = 0; u < 8; u++) {
+                        if constexpr (UNIT_W) acc = __dadd_rn(acc, (double)lv[u]);
+                        else acc = __dadd_rn(acc, __dmul_rn(__ldg(a.weight + ci.w + i + u),
+                                                            (double)lv[u]));
+                    }
+                }
+                for (; i < nt; i++) {
+                    const float lv = lbc[i * B + tid];
                     if constexpr (UNIT_W) acc = __dadd_rn(acc, (double)lv);
                     else acc = __dadd_rn(acc, __dmul_rn(__ldg(a.weight + ci.w + i), (double)lv));
                 }
             }
-            consumer_sync();  // leaf buffer free for the next chunk
         }
         if (tid < B && my_row < a.n) a.out[my_row] = acc;
     }
@@ -206,24 +243,28 @@ bool plan_cstream(int F, int device, CStreamArgs *a) {
     if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device) !=
         cudaSuccess)
         return false;
+    // Largest instance tile first; then the chain count K whose full round of
+    // S * K trees (one K-group per warp) fits a ring stage at ~1.2 KB/tree.
     for (int G = 8; G >= 1; G >>= 1) {
         const int B = 32 * G;
-        const size_t xs = ((size_t)(F + 1) * B * 4 + 127) & ~(size_t)127;
-        const size_t lb = (size_t)kCStreamMaxT * B * 4;
-        const size_t bars = 4 * 8;
-        if (xs + lb + bars >= (size_t)optin) continue;
-        const size_t cap = (((size_t)optin - xs - lb - bars) / kStagesC) & ~(size_t)127;
-        if (cap < 8 * 1024) continue;
-        a->B = B;
-        a->xs_bytes = (uint32_t)xs;
-        a->lb_bytes = (uint32_t)lb;
-        a->chunk_cap = (uint32_t)std::min<size_t>(cap, 64 * 1024);
-        // trees per chunk: whole rounds of (S subsets x K chains), <= kCStreamMaxT
         const int S = kWarps / G;
-        int tpc = S * kK;
-        while (tpc * 2 <= kCStreamMaxT) tpc *= 2;
-        a->tpc = tpc;
-        return true;
+        const size_t xs = ((size_t)(F + 1) * B * 4 + 127) & ~(size_t)127;
+        const size_t bars = 4 * 8;
+        for (int K = 8; K >= 4; K >>= 1) {
+            const int tpc = std::min(S * K, kCStreamMaxT);
+            const size_t lb = 2 * (size_t)tpc * B * 4;  // double-buffered
+            if (xs + lb + bars >= (size_t)optin) continue;
+            const size_t stage = ((((size_t)optin - xs - lb - bars) / kStagesC) & ~(size_t)127);
+            if (stage < kMetaBytes + (size_t)tpc * 1200) continue;
+            a->B = B;
+            a->k = K;
+            a->tpc = tpc;
+            a->xs_bytes = (uint32_t)xs;
+            a->lb_bytes = (uint32_t)lb;
+            a->stage_bytes = (uint32_t)std::min<size_t>(stage, 64 * 1024 + kMetaBytes);
+            a->chunk_cap = a->stage_bytes - kMetaBytes;  // tree bytes per stage
+            return true;
+        }
     }
     return false;
 }
@@ -231,12 +272,17 @@ bool plan_cstream(int F, int device, CStreamArgs *a) {
 cudaError_t launch_cstream(const CStreamArgs &a, int device, cudaStream_t stream) {
     using namespace cstream_detail;
     if (a.n <= 0) return cudaSuccess;
-    auto kern = a.ord ? (a.unit_w ? k_cstream<true, true> : k_cstream<false, true>)
-                      : (a.unit_w ? k_cstream<true, false> : k_cstream<false, false>);
+    auto pick = [&](auto kk) {
+        constexpr int K = decltype(kk)::value;
+        return a.ord ? (a.unit_w ? k_cstream<K, true, true> : k_cstream<K, false, true>)
+                     : (a.unit_w ? k_cstream<K, true, false> : k_cstream<K, false, false>);
+    };
+    auto kern = a.k == 8 ? pick(std::integral_constant<int, 8>{})
+                         : pick(std::integral_constant<int, 4>{});
     int sms = 0;
     cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     if (e != cudaSuccess) return e;
-    const size_t smem = (size_t)a.xs_bytes + a.lb_bytes + (size_t)kStagesC * a.chunk_cap + 4 * 8;
+    const size_t smem = (size_t)a.xs_bytes + a.lb_bytes + (size_t)kStagesC * a.stage_bytes + 4 * 8;
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const long long tiles = (a.n + a.B - 1) / a.B;

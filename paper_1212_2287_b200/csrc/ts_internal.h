@@ -170,7 +170,8 @@ struct CStreamArgs {
     const unsigned char *slot_inv;
     int chunk0, nchunks;
     int tpc;               // max trees per chunk
-    uint32_t chunk_cap, xs_bytes, lb_bytes;
+    int k;                 // lockstep chains per thread (4 or 8)
+    uint32_t chunk_cap, stage_bytes, xs_bytes, lb_bytes;
     const double *weight;
     int unit_w, accumulate;
     double *out;
