@@ -108,6 +108,15 @@ int ts_score(const ts_model *model, const float *x, int64_t n, int64_t f, int64_
              double *out, uint16_t *ord_out, int64_t ld_ord, int32_t *status,
              void *stream);
 
+/* ts_score with an incoming partial sum: when accumulate != 0, out[i] holds
+ * the f64 sum of the trees that precede this model's trees in evaluation
+ * order and scoring continues from it (acc = out[i]; acc = acc + w*leaf ...),
+ * so a tree-sharded ensemble scored shard after shard -- on one GPU or
+ * pipelined across GPUs -- reproduces the single-model sum bit for bit. */
+int ts_score_ex(const ts_model *model, const float *x, int64_t n, int64_t f, int64_t ld,
+                double *out, uint16_t *ord_out, int64_t ld_ord, int32_t *status,
+                int accumulate, void *stream);
+
 /* Host-buffer scoring: same argument meaning as the reference's generated
  * score_batch(x, n, f, out).  Copies x to the device in chunks on two
  * streams (H2D of chunk i+1 overlaps scoring of chunk i), copies the scores

@@ -104,11 +104,13 @@ def ordinals(tables, X) -> np.ndarray:
     return res
 
 
-def score(tables, weights, X, ords=None) -> np.ndarray:
-    """f64 tree-order sum ``acc += w * leaf64[ord]`` (starts at +0.0)."""
+def score(tables, weights, X, ords=None, init=None) -> np.ndarray:
+    """f64 tree-order sum ``acc += w * leaf64[ord]`` (starts at +0.0, or at
+    ``init`` -- the running sums of the trees before these, for tree shards)."""
     if ords is None:
         ords = ordinals(tables, X)
-    acc = np.zeros(ords.shape[1], dtype=np.float64)
+    acc = np.zeros(ords.shape[1], dtype=np.float64) if init is None \
+        else np.array(init, dtype=np.float64, copy=True)
     for t, (_d, _cf, _ct, cl) in enumerate(tables):
         acc += float(weights[t]) * cl.astype(np.float64)[ords[t]]
     return acc

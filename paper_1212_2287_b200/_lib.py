@@ -24,7 +24,7 @@ TS_ERR_NOMEM = 6
 TS_ERR_UNSUPPORTED = 7
 
 # Every symbol include/treescore_gpu.h declares (checked by the CPU tests).
-EXPORTS = ("ts_pack", "ts_model_get_info", "ts_score", "ts_score_host", "ts_free",
+EXPORTS = ("ts_pack", "ts_model_get_info", "ts_score", "ts_score_ex", "ts_score_host", "ts_free",
            "ts_last_error", "ts_launch_count", "ts_version", "ts_synth_uniform", "ts_set_kernel_path")
 
 
@@ -87,6 +87,8 @@ def load(build_if_missing: bool = True):
         lib.ts_model_get_info.restype = ctypes.c_int
         lib.ts_score.argtypes = [P, P, I64, I64, I64, P, P, I64, P, P]
         lib.ts_score.restype = ctypes.c_int
+        lib.ts_score_ex.argtypes = [P, P, I64, I64, I64, P, P, I64, P, ctypes.c_int, P]
+        lib.ts_score_ex.restype = ctypes.c_int
         lib.ts_score_host.argtypes = [P, P, I64, I64, P]
         lib.ts_score_host.restype = ctypes.c_int
         lib.ts_free.argtypes = [P]

@@ -55,7 +55,7 @@ struct DeviceGuard {
 
 int score_device(const ts_model *m, const float *x, int64_t n, int64_t f, int64_t ld,
                  double *out, uint16_t *ord, int64_t ld_ord, int32_t *status,
-                 cudaStream_t stream) {
+                 cudaStream_t stream, bool accumulate = false) {
     if (n == 0) return TS_OK;
     ScoreArgs a{};
     a.x = x;
@@ -76,7 +76,7 @@ int score_device(const ts_model *m, const float *x, int64_t n, int64_t f, int64_
         const Segment &seg = m->segments[s];
         a.t0 = seg.t0;
         a.t1 = seg.t1;
-        a.accumulate = s > 0;
+        a.accumulate = accumulate || s > 0;
         // Only the first launch of a call needs to flag non-finite input.
         a.status = s == 0 ? status : nullptr;
         cudaError_t e = launch_segment(seg, a, m->device, stream);
@@ -120,6 +120,18 @@ extern "C" int ts_score(const ts_model *m, const float *x, int64_t n, int64_t f,
     DeviceGuard g(m->device);
     if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
     return score_device(m, x, n, f, ld, out, ord_out, ld_ord, status, (cudaStream_t)stream);
+}
+
+extern "C" int ts_score_ex(const ts_model *m, const float *x, int64_t n, int64_t f, int64_t ld,
+                           double *out, uint16_t *ord_out, int64_t ld_ord, int32_t *status,
+                           int accumulate, void *stream) {
+    int rc = check_args(m, x, n, f, ld, out);
+    if (rc) return rc;
+    if (ord_out && ld_ord < n) return fail(TS_ERR_SHAPE, "ld_ord must be >= n");
+    DeviceGuard g(m->device);
+    if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
+    return score_device(m, x, n, f, ld, out, ord_out, ld_ord, status, (cudaStream_t)stream,
+                        accumulate != 0);
 }
 
 extern "C" int ts_score_host(const ts_model *mc, const float *x, int64_t n, int64_t f,

@@ -1,0 +1,173 @@
+"""Multi-GPU driver: one process per GPU, torch.distributed for the plumbing.
+
+SURVEY.md section 8(e): instances are independent, so the path shards two ways.
+
+* Instance sharding (configs 0-3, 4a): rank r owns the contiguous row range
+  :func:`row_shard`; every rank holds the whole packed ensemble; no collective
+  touches the data path.  Scores stay sharded (``gather_scores`` collects them
+  on one rank when a caller wants them in one place).
+* Tree sharding (config 4b, tables beyond L2): rank r owns the contiguous tree
+  range :func:`tree_shards` (balanced by sum of depths, global tree order kept)
+  and scores ALL rows against it.  Two ways to combine:
+    - ``"reduce"``: every rank scores from +0.0 and one NCCL sum
+      (``ncclFloat64``, NVLink/NVSwitch) adds the partials.  The cross-shard
+      sum order differs from the reference's sequential order, so scores agree
+      to ~1e-16 relative, not bit for bit.
+    - ``"pipeline"``: row chunks flow rank 0 -> 1 -> ... -> R-1; each rank
+      continues the f64 accumulation of the previous shard (``ts_score_ex``
+      with ``accumulate``) and sends the running sums on with point-to-point
+      NCCL send/recv.  Every addition happens in the reference's tree order,
+      so the final scores are bit-identical to single-GPU scoring; the cost is
+      (R - 1) chunk times of pipeline fill.
+
+The per-rank scorer is injected (``make_scorer``) so the same driver runs on
+GPUs (the CUDA library) and, in the CPU test-suite, under ``gloo`` with the
+oracle standing in for the kernel.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable
+
+import numpy as np
+
+from .model import FlatModel
+
+
+def row_shard(n: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous rows ``[a, b)`` of rank ``rank`` (sizes differ by at most 1)."""
+    return n * rank // world, n * (rank + 1) // world
+
+
+def tree_shards(depths, world: int) -> list[tuple[int, int]]:
+    """Split trees into ``world`` contiguous ranges with balanced sum of depths.
+
+    Node visits per instance are sum(d_t), so balancing the
+    depth sum balances the kernel time; every range is non-empty when
+    ``len(depths) >= world``.
+    """
+    depths = np.asarray(depths, dtype=np.float64)
+    T = len(depths)
+    if world < 1 or T < world:
+        raise ValueError(f"cannot split {T} trees over {world} ranks")
+    cost = np.maximum(depths, 1.0)          # depth-0 trees still cost a leaf read
+    cum = np.concatenate([[0.0], np.cumsum(cost)])
+    cuts = [0]
+    for r in range(1, world):
+        target = cum[-1] * r / world
+        c = int(np.searchsorted(cum, target))
+        c = min(max(c, cuts[-1] + 1), T - (world - r))
+        cuts.append(c)
+    cuts.append(T)
+    return [(cuts[i], cuts[i + 1]) for i in range(world)]
+
+
+@dataclass
+class ShardPlan:
+    mode: str                      # "instance" | "tree-reduce" | "tree-pipeline"
+    world: int
+    rank: int
+    rows: tuple[int, int]          # rows this rank scores
+    trees: tuple[int, int]         # trees this rank holds
+
+
+def plan(mode: str, n: int, flat: FlatModel, world: int, rank: int,
+         depths=None) -> ShardPlan:
+    if mode == "instance":
+        return ShardPlan(mode, world, rank, row_shard(n, world, rank), (0, flat.num_trees))
+    if mode in ("tree-reduce", "tree-pipeline"):
+        d = flat.depths() if depths is None else depths
+        return ShardPlan(mode, world, rank, (0, n), tree_shards(d, world)[rank])
+    raise ValueError(f"unknown shard mode {mode!r}")
+
+
+def gpu_scorer(flat: FlatModel, device: int):
+    """Default per-rank scorer: the CUDA library on ``device``.
+
+    Returns ``score(x, out, accumulate)`` over torch CUDA tensors.
+    """
+    from .evaluator import GpuModel
+    model = GpuModel(flat, device)
+
+    def score(x, out, accumulate=False):
+        model.score(x, out=out, accumulate=accumulate)
+        return out
+    score.model = model
+    return score
+
+
+class ShardedScorer:
+    """This rank's share of a sharded scoring job; packs its shard once.
+
+    ``x_local``: this rank's instances -- its row shard for ``"instance"``,
+    all ``n_total`` rows for the tree modes.  ``__call__`` returns the rank's
+    row-shard scores for ``"instance"``; for the tree modes the full f64
+    ``[n_total]`` scores land on rank 0 (``"tree-reduce"``) or on the last
+    rank (``"tree-pipeline"``), partial sums elsewhere.
+    """
+
+    def __init__(self, mode: str, flat: FlatModel, n_total: int, *, group=None,
+                 make_scorer: Callable | None = None, device=None, depths=None,
+                 chunk_rows: int = 1 << 17):
+        import torch.distributed as dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.n_total = n_total
+        self.chunk_rows = chunk_rows
+        self.plan = plan(mode, n_total, flat, self.world, self.rank, depths)
+        shard = flat if mode == "instance" else flat.subset(*self.plan.trees)
+        self.score = (make_scorer or (lambda fm: gpu_scorer(fm, device)))(shard)
+
+    def __call__(self, x_local, out=None):
+        import torch
+        import torch.distributed as dist
+        mode, rank, world, grp = self.plan.mode, self.rank, self.world, self.group
+        dev = x_local.device
+        if mode == "instance":
+            if out is None:
+                out = torch.empty(x_local.shape[0], dtype=torch.float64, device=dev)
+            self.score(x_local, out, False)
+            return out
+        if out is None:
+            out = torch.empty(self.n_total, dtype=torch.float64, device=dev)
+        if mode == "tree-reduce":
+            self.score(x_local, out, False)
+            dist.reduce(out, dst=0, op=dist.ReduceOp.SUM, group=grp)
+            return out
+        # tree-pipeline: chunk c visits ranks 0..R-1 in order; rank r receives
+        # the running sums of chunk c from r-1, continues them over its trees
+        # and sends them on.
+        for c0 in range(0, self.n_total, self.chunk_rows):
+            c1 = min(self.n_total, c0 + self.chunk_rows)
+            seg = out[c0:c1]
+            if rank > 0:
+                dist.recv(seg, src=rank - 1, group=grp)
+            self.score(x_local[c0:c1], seg, rank > 0)
+            if rank < world - 1:
+                dist.send(seg, dst=rank + 1, group=grp)
+        return out
+
+
+def run_sharded(mode: str, flat: FlatModel, x_local, n_total: int, **kw):
+    """One-shot :class:`ShardedScorer`; returns ``(plan, scores)``."""
+    sc = ShardedScorer(mode, flat, n_total, **kw)
+    return sc.plan, sc(x_local)
+
+
+def gather_scores(local, n_total: int, group=None, dst: int = 0):
+    """Collect instance-sharded scores on ``dst`` (not part of the hot path)."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    sizes = [row_shard(n_total, world, r) for r in range(world)]
+    width = max(b - a for a, b in sizes)
+    buf = torch.zeros(width, dtype=torch.float64, device=local.device)
+    buf[:local.shape[0]] = local
+    parts = [torch.empty_like(buf) for _ in range(world)] if rank == dst else None
+    dist.gather(buf, parts, dst=dst, group=group)
+    if rank != dst:
+        return None
+    return torch.cat([parts[r][:b - a] for r, (a, b) in enumerate(sizes)])

@@ -85,7 +85,7 @@ class GpuModel:
         self.num_features = int(flat.num_features)
         self.num_trees = int(flat.num_trees)
 
-    def score(self, x, out=None, ordinals=None, status=None, stream=None):
+    def score(self, x, out=None, ordinals=None, status=None, stream=None, accumulate=False):
         """Enqueue scoring of a CUDA float32 ``[n, f]`` tensor (row stride >= f).
 
         ``out``: f64 CUDA tensor ``[n]`` (allocated if None).  ``ordinals``:
@@ -93,6 +93,8 @@ class GpuModel:
         torch.uint16) receiving predicated leaf ordinals.  ``status``: optional
         int32 CUDA scalar OR-ed with 1 on non-finite input.  Returns ``out``.
         Stream-ordered on ``stream`` (default: torch's current stream).
+        ``accumulate``: ``out`` holds the partial sum of the preceding trees
+        (a tree shard); scoring continues from it (``ts_score_ex``).
         """
         torch = _torch()
         if x.dim() != 2 or x.dtype != torch.float32 or not x.is_cuda:
@@ -114,10 +116,11 @@ class GpuModel:
             ord_ptr = ctypes.c_void_p(ordinals.data_ptr())
         if stream is None:
             stream = torch.cuda.current_stream(x.device)
-        rc = self._lib.ts_score(self.handle, ctypes.c_void_p(x.data_ptr()), n, f, x.stride(0),
-                                ctypes.c_void_p(out.data_ptr()), ord_ptr, ld_ord,
-                                ctypes.c_void_p(status.data_ptr()) if status is not None else None,
-                                ctypes.c_void_p(stream.cuda_stream))
+        rc = self._lib.ts_score_ex(self.handle, ctypes.c_void_p(x.data_ptr()), n, f, x.stride(0),
+                                   ctypes.c_void_p(out.data_ptr()), ord_ptr, ld_ord,
+                                   ctypes.c_void_p(status.data_ptr()) if status is not None
+                                   else None, 1 if accumulate else 0,
+                                   ctypes.c_void_p(stream.cuda_stream))
         if rc != _lib.TS_OK:
             raise RuntimeError(f"ts_score failed ({rc}): {_lib.last_error()}")
         return out

@@ -355,6 +355,32 @@ class FlatModel(NamedTuple):
         """``(tree_off, weight, fid, value, left, right)``."""
         return tuple(self[1:])
 
+    def subset(self, t0: int, t1: int) -> "FlatModel":
+        """Trees ``[t0, t1)`` as their own FlatModel (a tree shard)."""
+        if not 0 <= t0 < t1 <= self.num_trees:
+            raise ValueError(f"bad tree range [{t0}, {t1}) of {self.num_trees}")
+        a, b = int(self.tree_off[t0]), int(self.tree_off[t1])
+        return FlatModel(self.num_features, self.tree_off[t0:t1 + 1] - a,
+                         self.weight[t0:t1], self.fid[a:b], self.value[a:b], self.left[a:b],
+                         self.right[a:b])
+
+    def depths(self) -> np.ndarray:
+        """Depth of every tree (longest root-to-leaf edge count)."""
+        out = np.zeros(self.num_trees, np.int64)
+        for t in range(self.num_trees):
+            a, b = int(self.tree_off[t]), int(self.tree_off[t + 1])
+            fid, lc, rc = self.fid[a:b], self.left[a:b], self.right[a:b]
+            level = np.array([0])
+            d = 0
+            while True:
+                inner = level[fid[level] >= 0]
+                if inner.size == 0:
+                    break
+                level = np.concatenate([lc[inner], rc[inner]])
+                d += 1
+            out[t] = d
+        return out
+
     def to_ensemble(self) -> "Ensemble":
         trees = []
         for t in range(self.num_trees):

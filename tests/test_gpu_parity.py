@@ -186,3 +186,20 @@ def test_launch_counter_advances():
     before = _lib.launch_count()
     ev.predict_batch(g["X"])
     assert _lib.launch_count() > before
+
+
+def test_tree_shards_continue_sum_bit_exact():
+    # ts_score_ex(accumulate=1): scoring tree shard after tree shard from the
+    # running sums reproduces single-model scores bit for bit (what the
+    # multi-GPU tree pipeline relies on), on every kernel path.
+    import torch
+    from paper_1212_2287_b200 import GpuModel, synth
+    from paper_1212_2287_b200.distributed import tree_shards
+    for w in (synth.config2(8, n=3000, trees=60), synth.config3(n=3000, trees=40)):
+        x = torch.from_numpy(w.rows(0, w.n)).cuda()
+        full = GpuModel(w.flat).score(x)
+        out = torch.empty_like(full)
+        for i, (a, b) in enumerate(tree_shards(w.flat.depths(), 3)):
+            GpuModel(w.flat.subset(a, b)).score(x, out=out, accumulate=i > 0)
+        torch.cuda.synchronize()
+        assert torch.equal(out, full)

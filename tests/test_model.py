@@ -121,3 +121,27 @@ def test_flat_model_round_trip():
     flat = ens.flat()
     assert flat.num_trees == len(ens.trees)
     assert serialize_model(flat.to_ensemble()) == serialize_model(ens)
+
+
+REF_SRC = "/root/reference/pkg/src"
+
+
+@pytest.mark.skipif(not __import__("os").path.isdir(REF_SRC), reason="reference not mounted")
+def test_adopts_reference_ensemble_objects():
+    # build_gpu accepts the reference's own Ensemble (duck-typed Node graphs);
+    # the adopted model must serialize exactly as the reference does.
+    import subprocess
+    import sys
+    code = (
+        "import sys; sys.dont_write_bytecode=True; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
+        "import numpy as np, treescore as ts\n"
+        "from paper_1212_2287_b200 import Ensemble, serialize_model\n"
+        "from treescore.synth import GenConfig, gen_tree\n"
+        "trees=[(gen_tree(GenConfig(depth=d, num_features=9, seed=d)), 0.5+d) for d in range(5)]\n"
+        "ref=ts.Ensemble(9, trees)\n"
+        "ours=Ensemble.from_reference(ref)\n"
+        "assert serialize_model(ours)==ts.serialize_model(ref)\n"
+        "print('ok')\n") % (REF_SRC, __import__("os").path.dirname(GOLDEN_DIR).rsplit("/tests", 1)[0])
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                         env={**__import__("os").environ, "PYTHONDONTWRITEBYTECODE": "1"})
+    assert out.stdout.strip() == "ok", out.stderr
