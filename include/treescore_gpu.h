@@ -51,7 +51,8 @@ typedef enum {
     TS_ERR_NONFINITE = 4,    /* instance matrix holds NaN or +-inf         */
     TS_ERR_CUDA = 5,         /* CUDA runtime failure (message has details) */
     TS_ERR_NOMEM = 6,
-    TS_ERR_UNSUPPORTED = 7
+    TS_ERR_UNSUPPORTED = 7,
+    TS_ERR_SYNTAX = 8        /* malformed model document (line/col set)    */
 } ts_status;
 
 #define TS_MAX_DEPTH 16
@@ -133,6 +134,28 @@ const char *ts_last_error(void);
 
 /* Number of scoring-kernel launches issued by this process so far. */
 int64_t ts_launch_count(void);
+
+/* Native parser for the text model format (ref model.py:416-602, grammar in
+ * the reference SPEC "External Interfaces").  On success *out holds the flat
+ * model (nodes in file-id order); on failure it still holds err_line /
+ * err_col for TS_ERR_SYNTAX.  Free with ts_flat_free in both cases.
+ * Semantic errors return TS_ERR_INVALID with the reference's messages. */
+typedef struct {
+    int32_t num_features;
+    int32_t num_trees;
+    int64_t num_nodes;
+    int64_t *tree_node_offset;   /* [num_trees + 1] */
+    double *tree_weight;         /* [num_trees] */
+    int32_t *node_fid;           /* [num_nodes], -1 = leaf */
+    float *node_value;
+    int32_t *node_left;
+    int32_t *node_right;
+    int32_t err_line;
+    int32_t err_col;
+} ts_flat_model;
+
+int ts_parse_model(const char *text, int64_t len, ts_flat_model **out);
+void ts_flat_free(ts_flat_model *model);
 
 /* Synthetic instances (BASELINE configs 3/4): fills rows [row0, row0+n) of a
  * counter-based uniform [0,1) matrix in place on the current device, with

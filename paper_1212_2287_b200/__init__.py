@@ -13,7 +13,8 @@ from .data import (DataFormatError, Dataset, as_feature_vector, fvec_header, rea
 from .evaluator import GpuEvaluator, GpuModel, StrategyKind, build, build_gpu
 from .model import (DUMMY_FID, DUMMY_THETA, MAX_DEPTH, CompleteTree, DepthLimitError,
                     Ensemble, FlatModel, ModelError, ModelSemanticError, ModelSyntaxError,
-                    Node, Tree, expand_to_complete, load_model, parse_model,
+                    Node, Tree, expand_to_complete, load_flat_model, load_model, parse_model,
+                    parse_model_native,
                     reference_predict, save_model, serialize_model, traverse_to_leaf,
                     tree_stats)
 from ._lib import NativeLibraryError
@@ -25,7 +26,7 @@ __all__ = [
     "DUMMY_THETA", "Ensemble", "FlatModel", "GpuEvaluator", "GpuModel", "MAX_DEPTH",
     "ModelError", "ModelSemanticError", "ModelSyntaxError", "NativeLibraryError", "Node",
     "StrategyKind", "Tree", "as_feature_vector", "build", "build_gpu", "expand_to_complete",
-    "fvec_header", "load_model", "parse_model", "read_fvec", "read_fvec_into",
+    "fvec_header", "load_flat_model", "load_model", "parse_model", "parse_model_native", "read_fvec", "read_fvec_into",
     "reference_predict", "save_model", "serialize_model", "traverse_to_leaf", "tree_stats",
     "write_fvec",
 ]

@@ -22,10 +22,12 @@ TS_ERR_NONFINITE = 4
 TS_ERR_CUDA = 5
 TS_ERR_NOMEM = 6
 TS_ERR_UNSUPPORTED = 7
+TS_ERR_SYNTAX = 8
 
 # Every symbol include/treescore_gpu.h declares (checked by the CPU tests).
 EXPORTS = ("ts_pack", "ts_model_get_info", "ts_score", "ts_score_ex", "ts_score_host", "ts_free",
-           "ts_last_error", "ts_launch_count", "ts_version", "ts_synth_uniform", "ts_set_kernel_path")
+           "ts_last_error", "ts_launch_count", "ts_version", "ts_synth_uniform", "ts_set_kernel_path",
+           "ts_parse_model", "ts_flat_free")
 
 
 class NativeLibraryError(RuntimeError):
@@ -41,6 +43,20 @@ class ModelDesc(ctypes.Structure):
                 ("node_value", ctypes.c_void_p),
                 ("node_left", ctypes.c_void_p),
                 ("node_right", ctypes.c_void_p)]
+
+
+class FlatModelC(ctypes.Structure):
+    _fields_ = [("num_features", ctypes.c_int32),
+                ("num_trees", ctypes.c_int32),
+                ("num_nodes", ctypes.c_int64),
+                ("tree_node_offset", ctypes.POINTER(ctypes.c_int64)),
+                ("tree_weight", ctypes.POINTER(ctypes.c_double)),
+                ("node_fid", ctypes.POINTER(ctypes.c_int32)),
+                ("node_value", ctypes.POINTER(ctypes.c_float)),
+                ("node_left", ctypes.POINTER(ctypes.c_int32)),
+                ("node_right", ctypes.POINTER(ctypes.c_int32)),
+                ("err_line", ctypes.c_int32),
+                ("err_col", ctypes.c_int32)]
 
 
 class ModelInfo(ctypes.Structure):
@@ -104,6 +120,11 @@ def load(build_if_missing: bool = True):
         lib.ts_synth_uniform.restype = ctypes.c_int
         lib.ts_set_kernel_path.argtypes = [ctypes.c_int]
         lib.ts_set_kernel_path.restype = ctypes.c_int
+        lib.ts_parse_model.argtypes = [ctypes.c_char_p, I64,
+                                       ctypes.POINTER(ctypes.POINTER(FlatModelC))]
+        lib.ts_parse_model.restype = ctypes.c_int
+        lib.ts_flat_free.argtypes = [ctypes.POINTER(FlatModelC)]
+        lib.ts_flat_free.restype = None
         for name in EXPORTS:
             getattr(lib, name)
         _lib = lib

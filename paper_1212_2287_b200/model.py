@@ -738,6 +738,43 @@ def _tree_from_defs(t: int, defs: dict) -> Tree:
                             arr[:, 2].astype(np.int64), arr[:, 3].astype(np.int64))
 
 
+def parse_model_native(text) -> FlatModel:
+    """Parse with the native parser (``ts_parse_model``) straight to a
+    :class:`FlatModel` -- no per-node Python objects (config 4b's 20,000-tree
+    files).  Same errors as :func:`parse_model`."""
+    import ctypes
+    from . import _lib
+    lib = _lib.load()
+    data = text.encode("utf-8") if isinstance(text, str) else bytes(text)
+    out = ctypes.POINTER(_lib.FlatModelC)()
+    rc = lib.ts_parse_model(data, len(data), ctypes.byref(out))
+    try:
+        if rc == _lib.TS_ERR_SYNTAX:
+            msg = _lib.last_error()
+            msg = msg.split(": ", 1)[1] if msg.startswith("line ") else msg
+            raise ModelSyntaxError(msg, out.contents.err_line, out.contents.err_col)
+        if rc == _lib.TS_ERR_INVALID:
+            raise ModelSemanticError(_lib.last_error())
+        if rc != _lib.TS_OK:
+            raise ModelError(f"ts_parse_model failed ({rc}): {_lib.last_error()}")
+        m = out.contents
+        T, n = m.num_trees, m.num_nodes
+        arr = lambda p, k, dt: np.ctypeslib.as_array(p, shape=(max(k, 1),))[:k].astype(dt)
+        return FlatModel(int(m.num_features), arr(m.tree_node_offset, T + 1, np.int64),
+                         arr(m.tree_weight, T, np.float64), arr(m.node_fid, n, np.int32),
+                         arr(m.node_value, n, np.float32), arr(m.node_left, n, np.int32),
+                         arr(m.node_right, n, np.int32))
+    finally:
+        if out:
+            lib.ts_flat_free(out)
+
+
+def load_flat_model(path) -> FlatModel:
+    """Read a model file with the native parser (see parse_model_native)."""
+    with open(path, "rb") as fh:
+        return parse_model_native(fh.read())
+
+
 def load_model(path) -> Ensemble:
     with open(path, "r", encoding="utf-8") as fh:
         return parse_model(fh.read())

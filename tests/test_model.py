@@ -145,3 +145,110 @@ def test_adopts_reference_ensemble_objects():
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
                          env={**__import__("os").environ, "PYTHONDONTWRITEBYTECODE": "1"})
     assert out.stdout.strip() == "ok", out.stderr
+
+
+def _native():
+    from paper_1212_2287_b200 import parse_model_native
+    from paper_1212_2287_b200.build import build
+    build()
+    return parse_model_native
+
+
+@pytest.mark.parametrize("name", GOLDEN_CASES)
+def test_native_parser_matches_python_parser(name):
+    text = open(f"{GOLDEN_DIR}/{name}.model.txt").read()
+    a = _native()(text)
+    b = parse_model(text).flat()
+    assert a.num_features == b.num_features
+    for x, y in zip(a.arrays(), b.arrays()):
+        assert x.dtype == y.dtype and np.array_equal(x, y)
+
+
+BAD_DOCS = [
+    "",
+    "# only a comment\n",
+    "ensemble 2\n",
+    "ensemble x 1\n",
+    "ensemble 0 1\ntree 1\nleaf 0 1\nend\n",
+    "ensemble 2 0\n",
+    "ensemble 2 1\n",
+    "ensemble 2 1\ntree\n",
+    "ensemble 2 1\ntree abc\nleaf 0 1\nend\n",
+    "ensemble 2 1\ntree 1.0\nnode 0 0 x 1 2\n",
+    "ensemble 2 1\ntree 1.0\nnode 0 -1 0.5 1 2\nleaf 1 0\nleaf 2 1\nend\n",
+    "ensemble 2 1\ntree 1.0\nnode 0 2 0.5 1 2\nleaf 1 0\nleaf 2 1\nend\n",
+    "ensemble 2 1\ntree 1.0\nnode 0 1 1e39 1 2\nleaf 1 0\nleaf 2 1\nend\n",
+    "ensemble 2 1\ntree 1.0\nnode 0 1 0.5 1 3\nleaf 1 0\nleaf 2 1\nend\n",
+    "ensemble 2 1\ntree 1.0\nnode 0 1 0.5 1 1\nleaf 1 0\nend\n",
+    "ensemble 2 1\ntree 1.0\nleaf 0 1\nleaf 0 2\nend\n",
+    "ensemble 2 1\ntree 1.0\nleaf 1 1\nend\n",
+    "ensemble 2 1\ntree 1.0\nleaf -1 1\nend\n",
+    "ensemble 2 1\ntree 1.0\nleaf 0 inf\nend\n",
+    "ensemble 2 1\ntree 1.0\nleaf 0 1\n",
+    "ensemble 2 1\ntree 1.0\nleaf 0 1\nend x\n",
+    "ensemble 2 1\ntree 1.0\nleaf 0 1\nend\nleaf 0 1\n",
+    "ensemble 2 1\ntree 1.0\nbranch 0 1\nend\n",
+    "ensemble 2 1\ntree inf\nleaf 0 1\nend\n",
+    "ensemble 2 2\ntree 1.0\nleaf 0 1\nend\n",
+    "ensemble 2 1\ntree 1.0\nnode 0 0 0.5 1 2\nnode 1 0 0.5 0 2\nleaf 2 1\nend\n",
+    "ensemble 2 1\ntree 1.0\nnode 0 0 0.5 1 2\nleaf 1 0\nleaf 2 1\nleaf 3 1\nend\n",
+]
+
+
+@pytest.mark.parametrize("doc", BAD_DOCS)
+def test_native_parser_errors_match_python(doc):
+    native = _native()
+    try:
+        parse_model(doc)
+        py = None
+    except (ModelSyntaxError, ModelSemanticError) as exc:
+        py = exc
+    try:
+        native(doc)
+        nat = None
+    except (ModelSyntaxError, ModelSemanticError) as exc:
+        nat = exc
+    assert type(py) is type(nat), (py, nat)
+    if isinstance(py, ModelSyntaxError):
+        assert (py.line, py.col) == (nat.line, nat.col)
+    assert str(py) == str(nat)
+
+
+def test_native_parser_accepts_python_number_forms():
+    doc = "ensemble 1_0 1\ntree +1_0.5\nnode 0 0 1e-3 1 2\nleaf 1 -0.0\nleaf 2 INF\nend\n"
+    with pytest.raises(ModelSemanticError):
+        _native()(doc)
+    doc = doc.replace("INF", "2.5")
+    a, b = _native()(doc), parse_model(doc).flat()
+    for x, y in zip(a.arrays(), b.arrays()):
+        assert np.array_equal(x, y)
+
+
+@pytest.mark.skipif(not __import__("os").path.isdir(REF_SRC), reason="reference not mounted")
+def test_native_parser_errors_match_reference_parser():
+    import json
+    import subprocess
+    import sys
+    code = ("import sys, json; sys.dont_write_bytecode=True; sys.path.insert(0, %r)\n"
+            "import treescore as ts\n"
+            "docs=json.load(sys.stdin); res=[]\n"
+            "for d in docs:\n"
+            "    try:\n"
+            "        ts.parse_model(d); res.append(None)\n"
+            "    except ts.ModelSyntaxError as e: res.append(['syntax', str(e), e.line, e.col])\n"
+            "    except ts.ModelSemanticError as e: res.append(['semantic', str(e)])\n"
+            "print(json.dumps(res))\n") % REF_SRC
+    out = subprocess.run([sys.executable, "-c", code], input=json.dumps(BAD_DOCS),
+                         capture_output=True, text=True,
+                         env={**__import__("os").environ, "PYTHONDONTWRITEBYTECODE": "1"})
+    ref = json.loads(out.stdout)
+    native = _native()
+    for doc, r in zip(BAD_DOCS, ref):
+        try:
+            native(doc)
+            got = None
+        except ModelSyntaxError as e:
+            got = ["syntax", str(e), e.line, e.col]
+        except ModelSemanticError as e:
+            got = ["semantic", str(e)]
+        assert got == r, doc
