@@ -95,6 +95,11 @@ typedef struct {
  * models with a message naming the tree. */
 int ts_pack(const ts_model_desc *desc, int device, ts_model **out);
 
+/* ts_pack with options: TS_PACK_TRACE also uploads the logical trees for
+ * ts_trace (16 bytes per node). */
+#define TS_PACK_TRACE 1
+int ts_pack_ex(const ts_model_desc *desc, int device, int flags, ts_model **out);
+
 int ts_model_get_info(const ts_model *model, ts_model_info *info);
 
 /* Score n instances already resident on the model's device.
@@ -117,6 +122,16 @@ int ts_score(const ts_model *model, const float *x, int64_t n, int64_t f, int64_
 int ts_score_ex(const ts_model *model, const float *x, int64_t n, int64_t f, int64_t ld,
                 double *out, uint16_t *ord_out, int64_t ld_ord, int32_t *status,
                 int accumulate, void *stream);
+
+/* Traced prediction (ref predict_ensemble_traced, evaluators.py:599-620, and
+ * measure_feature_coverage, bench.py:412-427) for a device batch: scores
+ * (nullable), LOGICAL left-to-right leaf ordinals [T][ld_ord] (nullable) and
+ * per-instance visited-feature bitsets visited[n][words] (nullable; bit fid
+ * of word fid/32), walking the logical trees (left iff x < theta).  Needs a
+ * model packed with TS_PACK_TRACE.  Stream-ordered. */
+int ts_trace(const ts_model *model, const float *x, int64_t n, int64_t f, int64_t ld,
+             double *out, uint16_t *leaf_ord, int64_t ld_ord, uint32_t *visited,
+             int32_t words, void *stream);
 
 /* Host-buffer scoring: same argument meaning as the reference's generated
  * score_batch(x, n, f, out).  Copies x to the device in chunks on two

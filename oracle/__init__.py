@@ -133,6 +133,38 @@ def score_linked(flat, X) -> np.ndarray:
     return out
 
 
+def trace(flat, X):
+    """Restates predict_ensemble_traced (ref evaluators.py:599-620) per row:
+    visited-feature bitsets ``uint32 [n, ceil(f/32)]`` (real splits only) and
+    logical left-to-right leaf ordinals ``[T, n]``."""
+    off, _w, fid, val, left, right = flat
+    X = np.asarray(X, dtype=np.float32)
+    n, f = X.shape
+    T = len(off) - 1
+    bits = np.zeros((n, (f + 31) // 32), np.uint32)
+    leaves = np.empty((T, n), np.int64)
+    for t in range(T):
+        o = int(off[t])
+        # left-to-right leaf numbering: depth-first, left child first
+        ordinal = {}
+        stack = [0]
+        while stack:
+            i = stack.pop()
+            if fid[o + i] < 0:
+                ordinal[i] = len(ordinal)
+            else:
+                stack.append(int(right[o + i]))
+                stack.append(int(left[o + i]))
+        for r in range(n):
+            i = 0
+            while fid[o + i] >= 0:
+                k = int(fid[o + i])
+                bits[r, k >> 5] |= np.uint32(1 << (k & 31))
+                i = int(left[o + i]) if float(X[r, k]) < float(val[o + i]) else int(right[o + i])
+            leaves[t, r] = ordinal[i]
+    return bits, leaves
+
+
 # ---------------------------------------------------------------------------
 # C restatement (ctypes)
 # ---------------------------------------------------------------------------

@@ -10,7 +10,8 @@ the native library ``_ts_gpu.so`` (C ABI ``include/treescore_gpu.h``) through
 
 from .data import (DataFormatError, Dataset, as_feature_vector, fvec_header, read_fvec,
                    read_fvec_into, write_fvec)
-from .evaluator import GpuEvaluator, GpuModel, StrategyKind, build, build_gpu
+from .evaluator import (CoverageReport, GpuEvaluator, GpuModel, StrategyKind, TracedPrediction,
+                        build, build_gpu)
 from .model import (DUMMY_FID, DUMMY_THETA, MAX_DEPTH, CompleteTree, DepthLimitError,
                     Ensemble, FlatModel, ModelError, ModelSemanticError, ModelSyntaxError,
                     Node, Tree, expand_to_complete, load_flat_model, load_model, parse_model,
@@ -22,7 +23,7 @@ from ._lib import NativeLibraryError
 __version__ = "0.1.0"
 
 __all__ = [
-    "CompleteTree", "DataFormatError", "Dataset", "DepthLimitError", "DUMMY_FID",
+    "CompleteTree", "CoverageReport", "TracedPrediction", "DataFormatError", "Dataset", "DepthLimitError", "DUMMY_FID",
     "DUMMY_THETA", "Ensemble", "FlatModel", "GpuEvaluator", "GpuModel", "MAX_DEPTH",
     "ModelError", "ModelSemanticError", "ModelSyntaxError", "NativeLibraryError", "Node",
     "StrategyKind", "Tree", "as_feature_vector", "build", "build_gpu", "expand_to_complete",

@@ -23,9 +23,10 @@ TS_ERR_CUDA = 5
 TS_ERR_NOMEM = 6
 TS_ERR_UNSUPPORTED = 7
 TS_ERR_SYNTAX = 8
+TS_PACK_TRACE = 1
 
 # Every symbol include/treescore_gpu.h declares (checked by the CPU tests).
-EXPORTS = ("ts_pack", "ts_model_get_info", "ts_score", "ts_score_ex", "ts_score_host", "ts_free",
+EXPORTS = ("ts_pack", "ts_pack_ex", "ts_trace", "ts_model_get_info", "ts_score", "ts_score_ex", "ts_score_host", "ts_free",
            "ts_last_error", "ts_launch_count", "ts_version", "ts_synth_uniform", "ts_set_kernel_path",
            "ts_parse_model", "ts_flat_free")
 
@@ -99,6 +100,11 @@ def load(build_if_missing: bool = True):
         P, I32, I64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
         lib.ts_pack.argtypes = [ctypes.POINTER(ModelDesc), ctypes.c_int, ctypes.POINTER(P)]
         lib.ts_pack.restype = ctypes.c_int
+        lib.ts_pack_ex.argtypes = [ctypes.POINTER(ModelDesc), ctypes.c_int, ctypes.c_int,
+                                   ctypes.POINTER(P)]
+        lib.ts_pack_ex.restype = ctypes.c_int
+        lib.ts_trace.argtypes = [P, P, I64, I64, I64, P, P, I64, P, I32, P]
+        lib.ts_trace.restype = ctypes.c_int
         lib.ts_model_get_info.argtypes = [P, ctypes.POINTER(ModelInfo)]
         lib.ts_model_get_info.restype = ctypes.c_int
         lib.ts_score.argtypes = [P, P, I64, I64, I64, P, P, I64, P, P]

@@ -47,6 +47,14 @@ struct Segment {
 //             leaves, padded to 16 bytes (so a run of equal-depth trees is a
 //             regular array the TMA streams chunk by chunk);
 //  kCompact:  n_t uint2 records (see Layout), padded to 16 bytes.
+// Logical node for the tracer (ts_trace.cu): fid -1 marks a leaf whose
+// `left` holds its left-to-right ordinal and `value` its leaf value.
+struct TraceNode {
+    int32_t fid;
+    float value;
+    int32_t left, right;  // tree-local node ids
+};
+
 struct DeviceTables {
     unsigned char *blob = nullptr;
     uint32_t *tree_off16 = nullptr;  // [T]
@@ -56,6 +64,9 @@ struct DeviceTables {
     uint4 *chunk_info = nullptr;     // {blob off / 16, bytes, trees, first tree}
     uint32_t *slot_meta = nullptr;   // [chunks][kCStreamMaxT] rec_off/8 | depth<<16 | rel<<21
     unsigned char *slot_inv = nullptr;  // [chunks][kCStreamMaxT] tree rel -> slot
+    // TS_PACK_TRACE only
+    TraceNode *trace_nodes = nullptr;
+    uint32_t *trace_base = nullptr;  // [T] first node of tree t
 };
 
 // kComplete records store fid << kFidShift: the byte offset of feature fid's

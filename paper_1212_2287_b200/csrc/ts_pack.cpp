@@ -210,6 +210,8 @@ void free_tables(DeviceTables *t) {
     cudaFree(t->tree_off16);
     cudaFree(t->depth);
     cudaFree(t->weight);
+    cudaFree(t->trace_nodes);
+    cudaFree(t->trace_base);
     cudaFree(t->chunk_info);
     cudaFree(t->slot_meta);
     cudaFree(t->slot_inv);
@@ -219,6 +221,10 @@ void free_tables(DeviceTables *t) {
 }  // namespace ts
 
 extern "C" int ts_pack(const ts_model_desc *d, int device, ts_model **out) {
+    return ts_pack_ex(d, device, 0, out);
+}
+
+extern "C" int ts_pack_ex(const ts_model_desc *d, int device, int flags, ts_model **out) {
     using namespace ts;
     if (!out) return fail(TS_ERR_INVALID, "out is NULL");
     *out = nullptr;
@@ -375,6 +381,37 @@ extern "C" int ts_pack(const ts_model_desc *d, int device, ts_model **out) {
     if (!rc) rc = upload(&m->dev.chunk_info, chunk_info);
     if (!rc) rc = upload(&m->dev.slot_meta, slot_meta);
     if (!rc) rc = upload(&m->dev.slot_inv, slot_inv);
+    if (!rc && (flags & TS_PACK_TRACE)) {
+        // logical trees for the tracer: file-order nodes, leaf ordinals left-to-right
+        std::vector<TraceNode> tn(d->tree_node_offset[T]);
+        std::vector<uint32_t> tbase(T);
+        for (int t = 0; t < T; t++) {
+            const int64_t o = d->tree_node_offset[t], n = d->tree_node_offset[t + 1] - o;
+            tbase[t] = (uint32_t)o;
+            for (int64_t i = 0; i < n; i++) {
+                TraceNode &x = tn[o + i];
+                x.fid = d->node_fid[o + i];
+                x.value = d->node_value[o + i];
+                x.left = x.fid >= 0 ? d->node_left[o + i] : 0;
+                x.right = x.fid >= 0 ? d->node_right[o + i] : 0;
+            }
+            int32_t ord = 0;  // depth-first, left child first
+            std::vector<int32_t> stack(1, 0);
+            while (!stack.empty()) {
+                int32_t i = stack.back();
+                stack.pop_back();
+                if (tn[o + i].fid < 0) {
+                    tn[o + i].left = ord++;
+                } else {
+                    stack.push_back(tn[o + i].right);
+                    stack.push_back(tn[o + i].left);
+                }
+            }
+        }
+        if (d->tree_node_offset[T] >= ((int64_t)1 << 32)) rc = fail(TS_ERR_UNSUPPORTED, "too many nodes to trace");
+        if (!rc) rc = upload(&m->dev.trace_nodes, tn);
+        if (!rc) rc = upload(&m->dev.trace_base, tbase);
+    }
     if (prev >= 0) cudaSetDevice(prev);
     if (rc) {
         free_tables(&m->dev);

@@ -23,6 +23,7 @@ from __future__ import annotations
 
 import ctypes
 import enum
+from dataclasses import dataclass
 
 import numpy as np
 
@@ -49,10 +50,30 @@ def _ptr(a) -> ctypes.c_void_p:
     return ctypes.c_void_p(a.ctypes.data)
 
 
+@dataclass(frozen=True)
+class TracedPrediction:
+    """ref evaluators.py:592-596: score, union of path feature ids, logical
+    left-to-right leaf ordinal per tree."""
+
+    score: float
+    visited_features: frozenset
+    visited_leaves: tuple
+
+
+@dataclass(frozen=True)
+class CoverageReport:
+    """ref bench.py:153-158: fraction of the feature space examined per
+    prediction (mean and population variance over instances)."""
+
+    mean_fraction: float
+    variance: float
+    num_instances: int
+
+
 class GpuModel:
     """Packed device tables of one ensemble on one GPU (``ts_pack``)."""
 
-    def __init__(self, model, device: int | None = None):
+    def __init__(self, model, device: int | None = None, trace: bool = False):
         torch = _torch()
         if not torch.cuda.is_available():
             raise _lib.NativeLibraryError("no CUDA device: the GPU scorer has no CPU fallback")
@@ -70,7 +91,8 @@ class GpuModel:
         desc = _lib.ModelDesc(int(flat.num_features), int(flat.num_trees),
                               *[a.ctypes.data for a in arrs])
         handle = ctypes.c_void_p()
-        rc = lib.ts_pack(ctypes.byref(desc), self.device, ctypes.byref(handle))
+        rc = lib.ts_pack_ex(ctypes.byref(desc), self.device, _lib.TS_PACK_TRACE if trace else 0,
+                            ctypes.byref(handle))
         if rc == _lib.TS_ERR_DEPTH:
             raise DepthLimitError(_lib.last_error())
         if rc == _lib.TS_ERR_INVALID:
@@ -116,7 +138,8 @@ class GpuModel:
             ord_ptr = ctypes.c_void_p(ordinals.data_ptr())
         if stream is None:
             stream = torch.cuda.current_stream(x.device)
-        rc = self._lib.ts_score_ex(self.handle, ctypes.c_void_p(x.data_ptr()), n, f, x.stride(0),
+        ld = x.stride(0) if n > 1 else f   # size-1 leading dims may carry stride 0
+        rc = self._lib.ts_score_ex(self.handle, ctypes.c_void_p(x.data_ptr()), n, f, ld,
                                    ctypes.c_void_p(out.data_ptr()), ord_ptr, ld_ord,
                                    ctypes.c_void_p(status.data_ptr()) if status is not None
                                    else None, 1 if accumulate else 0,
@@ -124,6 +147,21 @@ class GpuModel:
         if rc != _lib.TS_OK:
             raise RuntimeError(f"ts_score failed ({rc}): {_lib.last_error()}")
         return out
+
+    def trace(self, x, out=None, leaf_ord=None, visited=None, stream=None):
+        """``ts_trace`` on a CUDA float32 ``[n, f]`` tensor (model packed with trace=True)."""
+        torch = _torch()
+        n, f = x.shape
+        words = (self.num_features + 31) // 32
+        if stream is None:
+            stream = torch.cuda.current_stream(x.device)
+        p = lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None
+        ld = x.stride(0) if n > 1 else f
+        rc = self._lib.ts_trace(self.handle, p(x), n, f, ld, p(out), p(leaf_ord),
+                                leaf_ord.stride(0) if leaf_ord is not None else 0, p(visited),
+                                words, ctypes.c_void_p(stream.cuda_stream))
+        if rc != _lib.TS_OK:
+            raise RuntimeError(f"ts_trace failed ({rc}): {_lib.last_error()}")
 
     def score_host(self, matrix: np.ndarray, out: np.ndarray) -> None:
         """``ts_score_host``: host fp32 ``[n, f]`` -> host f64 ``[n]``."""
@@ -160,13 +198,14 @@ class GpuEvaluator:
 
     kind = StrategyKind.GPU_VPREDICATED
 
-    def __init__(self, ensemble, batch_size: int | None = None, device: int | None = None):
+    def __init__(self, ensemble, batch_size: int | None = None, device: int | None = None,
+                 trace: bool = False):
         if batch_size is not None:
             batch_size = int(batch_size)
             if batch_size < 1:
                 raise ValueError(f"batch_size must be >= 1, got {batch_size}")
         self.batch_size = batch_size
-        self.model = GpuModel(ensemble, device)
+        self.model = GpuModel(ensemble, device, trace=trace)
         self.num_features = self.model.num_features
         self.num_trees = self.model.num_trees
         self.device = self.model.device
@@ -247,6 +286,47 @@ class GpuEvaluator:
             raise ValueError("dataset contains non-finite values")
         return ords[:, :n].cpu().numpy().view(np.uint16).astype(np.int64)
 
+    # -- traced prediction (ref evaluators.py:599-620, bench.py:412-427) ---------
+
+    def trace_batch(self, data):
+        """``(scores f64[n], visited uint32[n, ceil(F/32)], leaves int64[T, n])``:
+        per-instance visited-feature bitsets and logical leaf ordinals."""
+        torch = _torch()
+        dev = torch.device("cuda", self.device)
+        if isinstance(data, torch.Tensor):
+            x = data.to(device=dev, dtype=torch.float32).contiguous()
+        else:
+            x = torch.from_numpy(self._coerce_matrix(data)).to(dev)
+        n = x.shape[0]
+        words = (self.num_features + 31) // 32
+        out = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
+        vis = torch.zeros((max(n, 1), words), dtype=torch.int32, device=dev)
+        ords = torch.empty((self.num_trees, max(n, 1)), dtype=torch.int16, device=dev)
+        if n:
+            self.model.trace(x, out=out, leaf_ord=ords, visited=vis)
+        return (out[:n].cpu().numpy(), vis[:n].cpu().numpy().view(np.uint32),
+                ords[:, :n].cpu().numpy().view(np.uint16).astype(np.int64))
+
+    def predict_traced(self, x) -> TracedPrediction:
+        x = np.ascontiguousarray(x, dtype=np.float32)
+        if x.ndim != 1 or x.shape[0] != self.num_features:
+            raise ValueError(f"feature vector has shape {x.shape}, expected ({self.num_features},)")
+        s, vis, leaves = self.trace_batch(x[None, :])
+        bits = np.unpackbits(vis[0].view(np.uint8), bitorder="little")[:self.num_features]
+        return TracedPrediction(float(s[0]), frozenset(np.flatnonzero(bits).tolist()),
+                                tuple(int(v) for v in leaves[:, 0]))
+
+    def feature_coverage(self, data) -> CoverageReport:
+        """Mean fraction of features examined per instance (ref bench.py:412-427)."""
+        matrix = data.matrix if isinstance(data, Dataset) else self._coerce_matrix(data)
+        n = matrix.shape[0]
+        if n == 0:
+            return CoverageReport(0.0, 0.0, 0)
+        _s, vis, _l = self.trace_batch(matrix)
+        counts = np.unpackbits(vis.view(np.uint8), axis=1, bitorder="little").sum(axis=1)
+        fractions = counts.astype(np.float64) / self.num_features
+        return CoverageReport(float(fractions.mean()), float(fractions.var()), n)
+
     def close(self):
         self.model.close()
 
@@ -254,11 +334,13 @@ class GpuEvaluator:
         return f"GpuEvaluator(kind={self.kind}, trees={self.num_trees}, device={self.device})"
 
 
-def build_gpu(ensemble, batch_size: int | None = None, device: int | None = None) -> GpuEvaluator:
-    """Pack ``ensemble`` (Ensemble, FlatModel or reference treescore Ensemble)."""
+def build_gpu(ensemble, batch_size: int | None = None, device: int | None = None,
+              trace: bool = False) -> GpuEvaluator:
+    """Pack ``ensemble`` (Ensemble, FlatModel or reference treescore Ensemble).
+    ``trace=True`` also uploads the logical trees for traced prediction."""
     if not isinstance(ensemble, (Ensemble, FlatModel)) and hasattr(ensemble, "trees"):
         ensemble = Ensemble.from_reference(ensemble)
-    return GpuEvaluator(ensemble, batch_size, device)
+    return GpuEvaluator(ensemble, batch_size, device, trace=trace)
 
 
 def build(ensemble, kind=StrategyKind.GPU_VPREDICATED, batch_size: int | None = None,

@@ -16,6 +16,11 @@ For every case this writes ``<case>.model.txt`` (the reference's
                                   ``batch_kernel(d)`` on ``expand_to_complete``
                                   (``evaluators.py:90-99``, ``model.py:315-349``)
 * ``depths``       int32 [T]
+* ``trace_bits``   uint32 [n, ceil(f/32)]  ``predict_ensemble_traced`` visited
+                                  feature ids as bitsets (``evaluators.py:599-620``)
+* ``trace_leaves`` int32 [T, n]   its logical left-to-right leaf ordinals
+* ``coverage``     float64 [2]    ``measure_feature_coverage`` mean, variance
+                                  (``bench.py:412-427``)
 
 The GPU parity tests and the oracle tests read these files; the reference is
 never needed at test time (it does not exist on the GPU box).
@@ -77,10 +82,22 @@ def save(name, ens, X):
             ords[t] = 0
         else:
             ords[t] = batch_kernel(ct.depth)(ct.fids, ct.thetas, X, rows)
+    words = (X.shape[1] + 31) // 32
+    tbits = np.zeros((X.shape[0], words), np.uint32)
+    tleaves = np.empty((T, X.shape[0]), np.int32)
+    for i in range(X.shape[0]):
+        tr = ts.predict_ensemble_traced(ens, X[i])
+        assert tr.score == scores[i]
+        for fid in tr.visited_features:
+            tbits[i, fid >> 5] |= np.uint32(1 << (fid & 31))
+        tleaves[:, i] = tr.visited_leaves
+    cov = ts.measure_feature_coverage(ens, ts.Dataset(X))
     with open(os.path.join(HERE, f"{name}.model.txt"), "w") as fh:
         fh.write(ts.serialize_model(ens))
     np.savez_compressed(os.path.join(HERE, f"{name}.npz"), X=X, scores=scores,
-                        scores_vpred=vpred, ordinals=ords, depths=depths)
+                        scores_vpred=vpred, ordinals=ords, depths=depths, trace_bits=tbits,
+                        trace_leaves=tleaves,
+                        coverage=np.array([cov.mean_fraction, cov.variance]))
     print(f"{name}: T={T} n={X.shape[0]} f={X.shape[1]} depths={sorted(set(depths.tolist()))}")
 
 

@@ -203,3 +203,21 @@ def test_tree_shards_continue_sum_bit_exact():
             GpuModel(w.flat.subset(a, b)).score(x, out=out, accumulate=i > 0)
         torch.cuda.synchronize()
         assert torch.equal(out, full)
+
+
+@pytest.mark.parametrize("name", GOLDEN_CASES)
+def test_traced_prediction_and_coverage(name):
+    # ref predict_ensemble_traced (evaluators.py:599-620) and
+    # measure_feature_coverage (bench.py:412-427), bit for bit
+    ens, g = load_golden(name)
+    ev = _ev(ens, trace=True)
+    scores, bits, leaves = ev.trace_batch(g["X"])
+    assert np.array_equal(scores, g["scores"])
+    assert np.array_equal(bits, g["trace_bits"])
+    assert np.array_equal(leaves, g["trace_leaves"])
+    cov = ev.feature_coverage(g["X"])
+    assert (cov.mean_fraction, cov.variance, cov.num_instances) == \
+        (g["coverage"][0], g["coverage"][1], g["X"].shape[0])
+    tp = ev.predict_traced(g["X"][0])
+    assert tp.score == g["scores"][0]
+    assert tp.visited_leaves == tuple(g["trace_leaves"][:, 0].tolist())

@@ -77,3 +77,14 @@ def test_f64_accumulation_order_is_tree_order():
     for v in leaves:
         expected += float(np.float32(v))
     assert s[0] == expected
+
+
+@pytest.mark.parametrize("name", GOLDEN_CASES)
+def test_trace_oracle_matches_reference(name):
+    ens, g = load_golden(name)
+    bits, leaves = oracle.trace(ens.flat().arrays(), g["X"])
+    assert np.array_equal(bits, g["trace_bits"])
+    assert np.array_equal(leaves, g["trace_leaves"])
+    counts = np.unpackbits(bits.view(np.uint8), axis=1, bitorder="little").sum(axis=1)
+    frac = counts / g["X"].shape[1]
+    assert frac.mean() == g["coverage"][0] and frac.var() == g["coverage"][1]
