@@ -286,6 +286,70 @@ class GpuEvaluator:
             raise ValueError("dataset contains non-finite values")
         return ords[:, :n].cpu().numpy().view(np.uint16).astype(np.int64)
 
+    # -- input pipeline ---------------------------------------
+
+    def predict_fvec(self, path, chunk_rows: int = 1 << 18) -> np.ndarray:
+        """Score an FVEC file (ref data.py:72-96) of any size, streaming it.
+
+        A reader thread fills one pinned host buffer from disk while the GPU
+        scores the other (``ts_score_host``: chunked H2D overlapped with the
+        kernels, ctypes releases the GIL), so file IO, PCIe and compute
+        overlap and N is not bounded by HBM.  Non-finite values raise
+        ``ValueError`` like ``read_fvec``.
+        """
+        import threading
+
+        from .data import fvec_header, read_fvec_into
+        torch = _torch()
+        count, f, _off = fvec_header(path)
+        if f != self.num_features:
+            raise ValueError(f"dataset has shape ({count}, {f}), expected (n, {self.num_features})")
+        out = np.empty(count, dtype=np.float64)
+        if count == 0:
+            return out
+        rows = max(1, min(chunk_rows, count))
+        bufs = [torch.empty((rows, f), dtype=torch.float32, pin_memory=True).numpy()
+                for _ in range(2)]
+        filled = [threading.Semaphore(0), threading.Semaphore(0)]
+        free = [threading.Semaphore(1), threading.Semaphore(1)]
+        got = [0, 0]
+        err = []
+        stop = threading.Event()
+
+        def reader():
+            try:
+                k = 0
+                for r0 in range(0, count, rows):
+                    free[k].acquire()
+                    if stop.is_set():
+                        return
+                    got[k] = read_fvec_into(path, bufs[k], r0)
+                    filled[k].release()
+                    k ^= 1
+            except Exception as exc:  # noqa: BLE001 - re-raised on the caller's thread
+                err.append(exc)
+                for sem in filled:
+                    sem.release()
+
+        th = threading.Thread(target=reader, daemon=True)
+        th.start()
+        k = 0
+        try:
+            for r0 in range(0, count, rows):
+                filled[k].acquire()
+                if err:
+                    raise err[0]
+                m = got[k]
+                self.model.score_host(bufs[k][:m], out[r0:r0 + m])
+                free[k].release()
+                k ^= 1
+        finally:
+            stop.set()
+            for sem in free:
+                sem.release()
+            th.join(timeout=60)
+        return out
+
     # -- traced prediction (ref evaluators.py:599-620, bench.py:412-427) ---------
 
     def trace_batch(self, data):

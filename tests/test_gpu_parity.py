@@ -221,3 +221,18 @@ def test_traced_prediction_and_coverage(name):
     tp = ev.predict_traced(g["X"][0])
     assert tp.score == g["scores"][0]
     assert tp.visited_leaves == tuple(g["trace_leaves"][:, 0].tolist())
+
+
+def test_predict_fvec_streams_files(tmp_path):
+    from paper_1212_2287_b200 import write_fvec
+    ens, g = load_golden("mixed")
+    ev = _ev(ens)
+    path = tmp_path / "x.fvec"
+    write_fvec(path, g["X"])
+    for chunk in (64, 333, 10_000):
+        assert np.array_equal(ev.predict_fvec(path, chunk_rows=chunk), g["scores"])
+    X = g["X"].copy()
+    X[401, 2] = np.nan
+    write_fvec(path, X)
+    with pytest.raises(ValueError, match="non-finite"):
+        ev.predict_fvec(path, chunk_rows=128)
