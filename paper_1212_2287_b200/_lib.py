@@ -12,7 +12,8 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(HERE, "_ts_gpu.so")
+# TS_GPU_SO overrides the library path (A/B timing of alternative builds).
+SO_PATH = os.environ.get("TS_GPU_SO") or os.path.join(HERE, "_ts_gpu.so")
 
 TS_OK = 0
 TS_ERR_INVALID = 1

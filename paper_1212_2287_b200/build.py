@@ -16,7 +16,7 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-SO = os.path.join(HERE, "_ts_gpu.so")
+SO = os.environ.get("TS_GPU_SO") or os.path.join(HERE, "_ts_gpu.so")
 SOURCES = ["ts_kernels.cu", "ts_stream.cu", "ts_stream_i0.cu", "ts_stream_i1.cu",
            "ts_stream_i2.cu", "ts_stream_i3.cu", "ts_stream_i4.cu", "ts_cstream.cu", "ts_trace.cu", "ts_synth.cu",
            "ts_pack.cpp", "ts_parse.cpp", "ts_capi.cpp"]
@@ -44,9 +44,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return SO
     from concurrent.futures import ThreadPoolExecutor
-    objdir = os.path.join(HERE, "build")
+    objdir = os.path.join(HERE, "build", os.path.basename(SO))
     os.makedirs(objdir, exist_ok=True)
-    common = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
+    common = [nvcc(), *ARCH, *os.environ.get("TS_NVCC_EXTRA", "").split(), "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
               "-Xptxas", "-warn-spills"]
     if verbose:
         common += ["-Xptxas", "-v"]

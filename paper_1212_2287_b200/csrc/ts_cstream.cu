@@ -146,9 +146,9 @@ __global__ void __launch_bounds__(kThreadsC, 1) k_cstream(CStreamArgs a) {
     uint32_t it = 0;
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const long long row0 = tile * B;
-        consumer_sync();
+        consumer_sync<kConsumers>();
         stage_rows_c(a, xs, row0);
-        consumer_sync();
+        consumer_sync<kConsumers>();
         const long long my_row = row0 + tid;  // accumulator owner (tid < B)
         double acc = (tid < B && my_row < a.n && a.accumulate) ? a.out[my_row] : 0.0;
         const long long walk_row = row0 + inst;
@@ -207,7 +207,7 @@ __global__ void __launch_bounds__(kThreadsC, 1) k_cstream(CStreamArgs a) {
             // One barrier per chunk: it publishes this chunk's leaf buffer and
             // frees its ring stage.  The other leaf buffer (written by the
             // next chunk) was last read before this barrier, so no second one.
-            consumer_sync();
+            consumer_sync<kConsumers>();
             if (tid == 0) mbar_arrive(empty + s);
             if (tid < B) {
                 const float *lbc = reinterpret_cast<const float *>(

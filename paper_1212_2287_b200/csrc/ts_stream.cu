@@ -55,19 +55,18 @@ const StreamFn kStreamTable[kStreamMaxDepth + 1] = {
 }  // namespace
 }  // namespace stream_detail
 
-int stream_instances_per_tile() { return stream_detail::kB; }
 
 // Shared-memory plan for a segment of depth D over F features; returns false
 // when the tile + two stages of at least K trees do not fit (the caller then
 // uses the L1 kernel).
-bool plan_stream(int F, int D, int device, StreamArgs *a) {
-    if (D > kStreamMaxDepth) return false;
-    int optin = 0;
-    if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device) !=
-        cudaSuccess)
-        return false;
+namespace {
+bool plan_stream_cw(int F, int D, int optin, int cw, StreamArgs *a) {
     using namespace stream_detail;
-    const size_t xs = ((size_t)F * kB * sizeof(float) + 127) & ~(size_t)127;
+    const int B = 32 * cw;
+    const int ctas = 256 / B;
+    // per-CTA budget when several CTAs share an SM (1 KB reserved per CTA)
+    if (ctas > 1) optin = std::min(optin, 228 * 1024 / ctas - 1024);
+    const size_t xs = ((size_t)F * B * sizeof(float) + 127) & ~(size_t)127;
     a->fw = split_fid_width(F);
     a->tree_bytes = split_geom(D, a->fw).bytes;
     const uint32_t tb = a->tree_bytes;
@@ -87,15 +86,31 @@ bool plan_stream(int F, int D, int device, StreamArgs *a) {
         stages = s;
         tpc = (uint32_t)(g * K);
     }
-    if (!stages) {  // not even two K-groups fit: two stages of single trees
-        stages = 2;
+    if (!stages) {
+        if (cw == 4) return false;  // the 256-row shape handles it better
+        stages = 2;                 // not even two K-groups fit: single trees
         tpc = (uint32_t)std::max<size_t>(1, (ring / 2) / tb);
     }
+    a->cw = cw;
     a->xs_bytes = (uint32_t)xs;
     a->tpc = (int)tpc;
     a->stages = stages;
     a->chunk_cap = (tpc * tb + 127) & ~127u;
     return true;
+}
+}  // namespace
+
+// Shared-memory plan for a segment of depth D over F features: two 128-row
+// CTAs per SM when a full ring of K-groups fits (d <= 9), else one 256-row
+// CTA; false when not even that fits (the caller uses the L1 kernel).
+bool plan_stream(int F, int D, int device, StreamArgs *a) {
+    if (D > kStreamMaxDepth) return false;
+    int optin = 0;
+    if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device) !=
+        cudaSuccess)
+        return false;
+    if (D <= 9 && plan_stream_cw(F, D, optin, 4, a)) return true;
+    return plan_stream_cw(F, D, optin, 8, a);
 }
 
 cudaError_t launch_stream(int D, const StreamArgs &a, int device, cudaStream_t stream) {

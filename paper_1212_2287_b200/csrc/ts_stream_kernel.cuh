@@ -34,9 +34,21 @@
 namespace ts {
 namespace stream_detail {
 
-constexpr int kConsumerWarps = 8;
-constexpr int kB = kConsumerWarps * 32;  // instances per tile
-constexpr int kThreads = kB + 32;        // + producer warp
+// CTA shape: CW consumer warps own a tile of B = 32*CW instances, plus one
+// producer warp.  CW = 8: one 256-row CTA per SM; CW = 4: two 128-row CTAs
+// per SM, so one CTA's x staging overlaps the other's walks (used when the
+// trees are small enough for the halved ring, d <= 9).
+template <int CW>
+struct Shape {
+    static constexpr int kConsumerWarps = CW;
+    static constexpr int kB = CW * 32;
+    static constexpr int kThreads = kB + 32;
+    static constexpr int kCtasPerSm = 256 / kB;
+    // Top-level records hold fid << kFidShift = byte offset in a 256-row
+    // x tile; a 128-row tile halves it.
+    static constexpr int kXShift = kB == 256 ? 0 : 1;
+};
+constexpr int kB = 256;  // the irregular-tree kernel's consumer count (ts_cstream.cu)
 constexpr int kMaxStages = 4;
 
 // Chains per thread by depth: deeper trees are bigger, so fewer fit in a
@@ -74,13 +86,16 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
         "l"(src), "r"(bytes), "r"(su32(bar))
         : "memory");
 }
+template <int NT = kB>
 __device__ __forceinline__ void consumer_sync() {
-    asm volatile("bar.sync 1, %0;" ::"n"(kB) : "memory");
+    asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
 }
 __device__ __forceinline__ bool finite_f(float v) { return fabsf(v) <= 3.402823466e38f; }
 
-// Transposing stage of B rows into xs[f * kB + r] (consumer threads only).
+// Transposing stage of B rows into xs[f * B + r] (consumer threads only).
+template <int B>
 __device__ __forceinline__ void stage_rows(const StreamArgs &a, float *xs, long long row0) {
+    constexpr int kB = B;
     const int r = threadIdx.x;
     const long long row = row0 + r;
     const bool valid = row < a.n;
@@ -152,7 +167,7 @@ __device__ __forceinline__ uint32_t ldsu(uint32_t addr, int fw) {
 //    state v = base_fid + FW * i (i = index within the level), the step
 //    i -> 2i + c becomes v -> 2v - base_fid + FW * c and the threshold sits at
 //    (4/FW) * v + kq + per-level immediate.
-template <int D, int NK, int FW, bool UNIT_W, bool ORD>
+template <int D, int NK, int FW, bool UNIT_W, bool ORD, int CW>
 __device__ __forceinline__ void walk_group(uint32_t tree0, uint32_t tree_bytes, uint32_t xr,
                                            double &acc, const StreamArgs &a, int t,
                                            long long row, bool valid) {
@@ -171,7 +186,7 @@ __device__ __forceinline__ void walk_group(uint32_t tree0, uint32_t tree_bytes, 
         for (int k = 0; k < NK; k++) {
             const uint32_t base = tree0 + k * tree_bytes;
             const uint2 q = lds64(p[k]);
-            const float v = ldsf(q.x + xr);
+            const float v = ldsf((q.x >> Shape<CW>::kXShift) + xr);
             p[k] = 2u * p[k] + (v >= __uint_as_float(q.y) ? 16u - base : 8u - base);
         }
     }
@@ -194,7 +209,7 @@ __device__ __forceinline__ void walk_group(uint32_t tree0, uint32_t tree_bytes, 
                 const uint32_t kq = base + kThr0 - (bf << kShift);
                 const float th = ldsf((idx[k] << kShift) + kq + 4u * lvl);
                 const uint32_t fid = ldsu(idx[k] + FW * lvl, FW);
-                const float v = ldsf(fid * (kB * 4u) + xr);
+                const float v = ldsf(fid * (Shape<CW>::kB * 4u) + xr);
                 idx[k] = 2u * idx[k] + (v >= th ? (uint32_t)FW - bf : 0u - bf);
             }
         }
@@ -217,8 +232,11 @@ __device__ __forceinline__ void walk_group(uint32_t tree0, uint32_t tree_bytes, 
     }
 }
 
-template <int D, int K, int FW, bool UNIT_W, bool ORD>
-__global__ void __launch_bounds__(kThreads, 1) k_stream(StreamArgs a) {
+template <int D, int K, int FW, bool UNIT_W, bool ORD, int CW>
+__global__ void __launch_bounds__(Shape<CW>::kThreads, Shape<CW>::kCtasPerSm)
+    k_stream(StreamArgs a) {
+    constexpr int kB = Shape<CW>::kB;
+    constexpr int kConsumerWarps = CW;
     extern __shared__ __align__(128) unsigned char smem[];
     float *xs = reinterpret_cast<float *>(smem);
     unsigned char *ring = smem + a.xs_bytes;
@@ -264,9 +282,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_stream(StreamArgs a) {
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const long long row = tile * kB + r;
         const bool valid = row < a.n;
-        consumer_sync();  // previous tile's walks are done with xs
-        stage_rows(a, xs, tile * kB);
-        consumer_sync();
+        consumer_sync<kB>();  // previous tile's walks are done with xs
+        stage_rows<kB>(a, xs, tile * kB);
+        consumer_sync<kB>();
         double acc = (a.accumulate && valid) ? a.out[row] : 0.0;
         for (int c = 0; c < nchunks; c++, it++) {
             const int s = it % kStages;
@@ -276,11 +294,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_stream(StreamArgs a) {
             const int trees = min(a.tpc, a.t1 - t0);
             int k = 0;
             for (; k + K <= trees; k += K)
-                walk_group<D, K, FW, UNIT_W, ORD>(buf + k * a.tree_bytes, a.tree_bytes, xr, acc,
-                                                  a, t0 + k, row, valid);
+                walk_group<D, K, FW, UNIT_W, ORD, CW>(buf + k * a.tree_bytes, a.tree_bytes, xr,
+                                                      acc, a, t0 + k, row, valid);
             for (; k < trees; k++)
-                walk_group<D, 1, FW, UNIT_W, ORD>(buf + k * a.tree_bytes, a.tree_bytes, xr, acc,
-                                                  a, t0 + k, row, valid);
+                walk_group<D, 1, FW, UNIT_W, ORD, CW>(buf + k * a.tree_bytes, a.tree_bytes, xr,
+                                                      acc, a, t0 + k, row, valid);
             __syncwarp();
             if (lane == 0) mbar_arrive(empty + s);
         }
@@ -288,16 +306,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_stream(StreamArgs a) {
     }
 }
 
-template <int D, int FW>
+template <int D, int FW, int CW>
 auto pick_kernel(const StreamArgs &a) {
     constexpr int K = chains_for_depth(D);
-    if (a.ord) return a.unit_w ? k_stream<D, K, FW, true, true> : k_stream<D, K, FW, false, true>;
-    return a.unit_w ? k_stream<D, K, FW, true, false> : k_stream<D, K, FW, false, false>;
+    if (a.ord)
+        return a.unit_w ? k_stream<D, K, FW, true, true, CW> : k_stream<D, K, FW, false, true, CW>;
+    return a.unit_w ? k_stream<D, K, FW, true, false, CW> : k_stream<D, K, FW, false, false, CW>;
 }
 
-template <int D>
-cudaError_t launch_d(const StreamArgs &a, int device, cudaStream_t stream) {
-    auto kern = a.fw == 1 ? pick_kernel<D, 1>(a) : pick_kernel<D, 2>(a);
+template <int D, int CW>
+cudaError_t launch_dc(const StreamArgs &a, int device, cudaStream_t stream) {
+    constexpr int kB = Shape<CW>::kB;
+    constexpr int kCtasPerSm = Shape<CW>::kCtasPerSm;
+    constexpr int kThreads = Shape<CW>::kThreads;
+    auto kern = a.fw == 1 ? pick_kernel<D, 1, CW>(a) : pick_kernel<D, 2, CW>(a);
     int sms = 0;
     cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     if (e != cudaSuccess) return e;
@@ -305,10 +327,15 @@ cudaError_t launch_d(const StreamArgs &a, int device, cudaStream_t stream) {
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const long long tiles = (a.n + kB - 1) / kB;
-    const int grid = (int)(tiles < sms ? tiles : sms);
+    const int grid = (int)(tiles < (long long)sms * kCtasPerSm ? tiles : (long long)sms * kCtasPerSm);
     kern<<<grid, kThreads, smem, stream>>>(a);
     count_launch();
     return cudaGetLastError();
+}
+
+template <int D>
+cudaError_t launch_d(const StreamArgs &a, int device, cudaStream_t stream) {
+    return a.cw == 4 ? launch_dc<D, 4>(a, device, stream) : launch_dc<D, 8>(a, device, stream);
 }
 
 }  // namespace stream_detail
