@@ -141,7 +141,7 @@ struct ScoreArgs {
 };
 
 // Arguments of the shared-memory streaming kernel (ts_stream.cu).
-constexpr int kStreamMaxDepth = 11;
+constexpr int kStreamMaxDepth = 12;
 struct StreamArgs {
     int cw;                        // consumer warps per CTA (4: 2 CTAs/SM, 8: 1)
     int fw;                        // deep fid width in bytes (1: F <= 256, else 2)

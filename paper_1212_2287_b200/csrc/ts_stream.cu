@@ -45,12 +45,13 @@ extern template cudaError_t launch_d<8>(const StreamArgs &, int, cudaStream_t);
 extern template cudaError_t launch_d<9>(const StreamArgs &, int, cudaStream_t);
 extern template cudaError_t launch_d<10>(const StreamArgs &, int, cudaStream_t);
 extern template cudaError_t launch_d<11>(const StreamArgs &, int, cudaStream_t);
+extern template cudaError_t launch_d<12>(const StreamArgs &, int, cudaStream_t);
 
 namespace {
 using StreamFn = cudaError_t (*)(const StreamArgs &, int, cudaStream_t);
 const StreamFn kStreamTable[kStreamMaxDepth + 1] = {
     launch_d<0>, launch_d<1>, launch_d<2>, launch_d<3>, launch_d<4>, launch_d<5>,
-    launch_d<6>, launch_d<7>, launch_d<8>, launch_d<9>, launch_d<10>, launch_d<11>};
+    launch_d<6>, launch_d<7>, launch_d<8>, launch_d<9>, launch_d<10>, launch_d<11>, launch_d<12>};
 
 }  // namespace
 }  // namespace stream_detail

@@ -53,7 +53,9 @@ constexpr int kMaxStages = 4;
 
 // Chains per thread by depth: deeper trees are bigger, so fewer fit in a
 // ring stage (a K-group must fit one stage).
-__host__ __device__ constexpr int chains_for_depth(int d) { return d <= 9 ? 8 : d == 10 ? 4 : 2; }
+__host__ __device__ constexpr int chains_for_depth(int d) {
+    return d <= 9 ? 8 : d == 10 ? 4 : d == 11 ? 2 : 1;
+}
 
 __device__ __forceinline__ uint32_t su32(const void *p) {
     return (uint32_t)__cvta_generic_to_shared(p);
