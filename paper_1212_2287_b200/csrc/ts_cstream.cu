@@ -38,9 +38,10 @@ using namespace stream_detail;
 
 constexpr int kWarps = 8;
 constexpr int kConsumers = kWarps * 32;
-constexpr int kThreadsC = kConsumers + 32;
+constexpr int kThreadsC = kConsumers + 64;  // + accumulator warp + producer warp
 constexpr int kStagesC = 2;
 constexpr uint32_t kMetaBytes = kCStreamMaxT * 4;  // slot table at the head of a stage
+constexpr uint32_t kHeadBytes = kMetaBytes + 16;   // + the chunk's chunk_info entry
 
 // Stage B rows x F features into xs[f * B + r] (+ sentinel row F = -inf),
 // all 256 consumer threads cooperating.
@@ -99,21 +100,28 @@ __global__ void __launch_bounds__(kThreadsC, 1) k_cstream(CStreamArgs a) {
     float *lb0 = reinterpret_cast<float *>(smem + a.xs_bytes);  // two leaf buffers
     unsigned char *ring = smem + a.xs_bytes + a.lb_bytes;
     uint64_t *full = reinterpret_cast<uint64_t *>(ring + kStagesC * a.stage_bytes);
-    uint64_t *empty = full + kStagesC;
+    uint64_t *empty = full + kStagesC;  // ring stage consumed (8 walker warps)
+    uint64_t *lbf = empty + kStagesC;   // leaf buffer written (8 walker warps)
+    uint64_t *lbe = lbf + 2;            // leaf buffer folded (accumulator warp)
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStagesC; s++) {
             mbar_init(full + s, 1);
-            mbar_init(empty + s, 1);
+            mbar_init(empty + s, kWarps);
+        }
+        for (int b = 0; b < 2; b++) {
+            mbar_init(lbf + b, kWarps);
+            mbar_init(lbe + b, 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
     const int B = a.B;
     const long long ntiles = (a.n + B - 1) / B;
+    const uint32_t lb_half = a.lb_bytes / 2;
 
-    if (warp == kWarps) {  // ---- producer: one TMA bulk copy per chunk
+    if (warp == kWarps + 1) {  // ---- producer: TMA bulk copies per chunk
         if (lane == 0) {
             uint32_t it = 0;
             for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -122,18 +130,60 @@ __global__ void __launch_bounds__(kThreadsC, 1) k_cstream(CStreamArgs a) {
                     if (it >= kStagesC) mbar_wait(empty + s, ((it / kStagesC) - 1) & 1);
                     const uint4 ci = __ldg(a.chunk_info + a.chunk0 + c);
                     unsigned char *stage = ring + s * a.stage_bytes;
-                    mbar_expect_tx(full + s, ci.y + kMetaBytes);
+                    mbar_expect_tx(full + s, ci.y + kMetaBytes + 16);
                     bulk_g2s(stage, a.slot_meta + (size_t)(a.chunk0 + c) * kCStreamMaxT,
                              kMetaBytes, full + s);
-                    bulk_g2s(stage + kMetaBytes, a.blob + 16ull * ci.x, ci.y, full + s);
+                    bulk_g2s(stage + kMetaBytes, a.chunk_info + a.chunk0 + c, 16, full + s);
+                    bulk_g2s(stage + kHeadBytes, a.blob + 16ull * ci.x, ci.y, full + s);
                 }
             }
         }
         return;
     }
 
-    // ---- consumers
-    const int tid = threadIdx.x;
+    if (warp == kWarps) {  // ---- accumulator: folds leaves in TREE order
+        const int G = B >> 5;
+        uint32_t it = 0;
+        for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            const long long row0 = tile * B;
+            double acc[8];
+#pragma unroll
+            for (int g = 0; g < 8; g++) {
+                const long long row = row0 + g * 32 + lane;
+                acc[g] = (g < G && a.accumulate && row < a.n) ? a.out[row] : 0.0;
+            }
+            for (int c = 0; c < a.nchunks; c++, it++) {
+                const uint4 ci = __ldg(a.chunk_info + a.chunk0 + c);
+                const int nt = (int)ci.z;
+                const int b = it & 1;
+                mbar_wait(lbf + b, (it >> 1) & 1);
+                const float *lbc = reinterpret_cast<const float *>(
+                    reinterpret_cast<const unsigned char *>(lb0) + b * lb_half);
+                for (int i = 0; i < nt; i++) {
+                    double w = 1.0;
+                    if constexpr (!UNIT_W) w = __ldg(a.weight + ci.w + i);
+#pragma unroll
+                    for (int g = 0; g < 8; g++) {
+                        if (g < G) {
+                            const double lv = (double)lbc[i * B + g * 32 + lane];
+                            acc[g] = UNIT_W ? __dadd_rn(acc[g], lv)
+                                            : __dadd_rn(acc[g], __dmul_rn(w, lv));
+                        }
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(lbe + b);
+            }
+#pragma unroll
+            for (int g = 0; g < 8; g++) {
+                const long long row = row0 + g * 32 + lane;
+                if (g < G && row < a.n) a.out[row] = acc[g];
+            }
+        }
+        return;
+    }
+
+    // ---- walkers (8 warps)
     const int G = B >> 5;
     const int grp = warp % G;
     const int S = kWarps / G;
@@ -142,26 +192,26 @@ __global__ void __launch_bounds__(kThreadsC, 1) k_cstream(CStreamArgs a) {
     const uint32_t xr = su32(xs) + 4u * inst;
     const uint32_t B4 = 4u * B;
     const uint32_t lbase0 = su32(lb0);
-    const uint32_t lb_half = a.lb_bytes / 2;
     uint32_t it = 0;
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const long long row0 = tile * B;
-        consumer_sync<kConsumers>();
+        consumer_sync<kConsumers>();  // all walks of the previous tile are done
         stage_rows_c(a, xs, row0);
         consumer_sync<kConsumers>();
-        const long long my_row = row0 + tid;  // accumulator owner (tid < B)
-        double acc = (tid < B && my_row < a.n && a.accumulate) ? a.out[my_row] : 0.0;
         const long long walk_row = row0 + inst;
         const bool walk_valid = walk_row < a.n;
         for (int c = 0; c < a.nchunks; c++, it++) {
             const int s = it % kStagesC;
-            const uint4 ci = __ldg(a.chunk_info + a.chunk0 + c);
-            const int nt = (int)ci.z;
-            const uint32_t lbase = lbase0 + (it & 1) * lb_half;
+            const int b = it & 1;
+            const uint32_t lbase = lbase0 + b * lb_half;
             mbar_wait(full + s, (it / kStagesC) & 1);
             const uint32_t meta = su32(ring + s * a.stage_bytes);
-            const uint32_t buf = meta + kMetaBytes;
-            for (int s0 = sub; s0 < nt; s0 += S * kK) {
+            uint32_t nt, tree0;
+            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(nt), "=r"(tree0)
+                         : "r"(meta + kMetaBytes + 8));  // chunk_info .z/.w
+            const uint32_t buf = meta + kHeadBytes;
+            bool waited = it < 2;  // this leaf buffer's previous fold must be done
+            for (int s0 = sub; s0 < (int)nt; s0 += S * kK) {
                 uint32_t p[kK], tb[kK], ob[kK], rel[kK];
                 int dk[kK];
                 int dmax = 0;
@@ -170,7 +220,7 @@ __global__ void __launch_bounds__(kThreadsC, 1) k_cstream(CStreamArgs a) {
                     const int slot = s0 + k * S;
                     uint32_t m;
                     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(m)
-                                 : "r"(meta + 4u * (slot < nt ? slot : s0)));
+                                 : "r"(meta + 4u * (slot < (int)nt ? slot : s0)));
                     rel[k] = m >> 21;
                     tb[k] = buf + 8u * (m & 0xffffu);
                     p[k] = tb[k];
@@ -189,49 +239,32 @@ __global__ void __launch_bounds__(kThreadsC, 1) k_cstream(CStreamArgs a) {
                         if constexpr (ORD) ob[k] = 2u * ob[k] + (c ? 1u : 0u);
                     }
                 }
+                if (!waited) {
+                    mbar_wait(lbe + b, ((it >> 1) - 1) & 1);
+                    waited = true;
+                }
 #pragma unroll
                 for (int k = 0; k < kK; k++) {
                     const int slot = s0 + k * S;
-                    if (slot < nt) {
+                    if (slot < (int)nt) {
                         const float lv = ldsf(p[k] + 4u);
                         asm volatile("st.shared.f32 [%0], %1;" ::"r"(lbase + 4u * (rel[k] * B + inst)),
                                      "f"(lv));
                         if constexpr (ORD) {
                             if (walk_valid)
-                                a.ord[(long long)(ci.w + rel[k]) * a.ld_ord + walk_row] =
+                                a.ord[(long long)(tree0 + rel[k]) * a.ld_ord + walk_row] =
                                     (uint16_t)(ob[k] >> (dmax - dk[k]));
                         }
                     }
                 }
             }
-            // One barrier per chunk: it publishes this chunk's leaf buffer and
-            // frees its ring stage.  The other leaf buffer (written by the
-            // next chunk) was last read before this barrier, so no second one.
-            consumer_sync<kConsumers>();
-            if (tid == 0) mbar_arrive(empty + s);
-            if (tid < B) {
-                const float *lbc = reinterpret_cast<const float *>(
-                    reinterpret_cast<const unsigned char *>(lb0) + (it & 1) * lb_half);
-                int i = 0;
-                for (; i + 8 <= nt; i += 8) {
-                    float lv[8];
-#pragma unroll
-                    for (int u = 0; u < 8; u++) lv[u] = lbc[(i + u) * B + tid];
-#pragma unroll
-                    for (int u = 0; u < 8; u++) {
-                        if constexpr (UNIT_W) acc = __dadd_rn(acc, (double)lv[u]);
-                        else acc = __dadd_rn(acc, __dmul_rn(__ldg(a.weight + ci.w + i + u),
-                                                            (double)lv[u]));
-                    }
-                }
-                for (; i < nt; i++) {
-                    const float lv = lbc[i * B + tid];
-                    if constexpr (UNIT_W) acc = __dadd_rn(acc, (double)lv);
-                    else acc = __dadd_rn(acc, __dmul_rn(__ldg(a.weight + ci.w + i), (double)lv));
-                }
+            if (!waited) mbar_wait(lbe + b, ((it >> 1) - 1) & 1);
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(empty + s);  // ring stage read
+                mbar_arrive(lbf + b);    // leaves published (release orders the stores)
             }
         }
-        if (tid < B && my_row < a.n) a.out[my_row] = acc;
     }
 }
 
@@ -249,20 +282,20 @@ bool plan_cstream(int F, int device, CStreamArgs *a) {
         const int B = 32 * G;
         const int S = kWarps / G;
         const size_t xs = ((size_t)(F + 1) * B * 4 + 127) & ~(size_t)127;
-        const size_t bars = 4 * 8;
         for (int K = 8; K >= 4; K >>= 1) {
             const int tpc = std::min(S * K, kCStreamMaxT);
             const size_t lb = 2 * (size_t)tpc * B * 4;  // double-buffered
+            const size_t bars = 8 * 8;
             if (xs + lb + bars >= (size_t)optin) continue;
             const size_t stage = ((((size_t)optin - xs - lb - bars) / kStagesC) & ~(size_t)127);
-            if (stage < kMetaBytes + (size_t)tpc * 1200) continue;
+            if (stage < kHeadBytes + (size_t)tpc * 1200) continue;
             a->B = B;
             a->k = K;
             a->tpc = tpc;
             a->xs_bytes = (uint32_t)xs;
             a->lb_bytes = (uint32_t)lb;
-            a->stage_bytes = (uint32_t)std::min<size_t>(stage, 64 * 1024 + kMetaBytes);
-            a->chunk_cap = a->stage_bytes - kMetaBytes;  // tree bytes per stage
+            a->stage_bytes = (uint32_t)std::min<size_t>(stage, 64 * 1024 + kHeadBytes);
+            a->chunk_cap = a->stage_bytes - kHeadBytes;  // tree bytes per stage
             return true;
         }
     }
@@ -282,7 +315,7 @@ cudaError_t launch_cstream(const CStreamArgs &a, int device, cudaStream_t stream
     int sms = 0;
     cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     if (e != cudaSuccess) return e;
-    const size_t smem = (size_t)a.xs_bytes + a.lb_bytes + (size_t)kStagesC * a.stage_bytes + 4 * 8;
+    const size_t smem = (size_t)a.xs_bytes + a.lb_bytes + (size_t)kStagesC * a.stage_bytes + 8 * 8;
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const long long tiles = (a.n + a.B - 1) / a.B;
