@@ -44,7 +44,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return SO
     from concurrent.futures import ThreadPoolExecutor
-    objdir = os.path.join(HERE, "build", os.path.basename(SO))
+    import tempfile
+    objdir = os.path.join(tempfile.gettempdir(), "ts_gpu_build", os.path.basename(SO))
     os.makedirs(objdir, exist_ok=True)
     common = [nvcc(), *ARCH, *os.environ.get("TS_NVCC_EXTRA", "").split(), "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
               "-Xptxas", "-warn-spills"]
