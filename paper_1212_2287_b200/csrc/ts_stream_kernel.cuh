@@ -142,18 +142,41 @@ __device__ __forceinline__ void stage_rows(const StreamArgs &a, float *xs, long 
     if (bad && a.status) atomicOr(a.status, 1);
 }
 
+#ifdef TS_DEBUG
+// Debug builds (TS_NVCC_EXTRA=-DTS_DEBUG): every shared load of the walk is
+// bounds-checked against the CTA's shared allocation and traps (device-side
+// assert) on a violation.  compute-sanitizer is unavailable on this pool, so
+// this is the memory-safety net for the parity suite.
+__device__ __forceinline__ void dbg_check(uint32_t addr, uint32_t width) {
+    uint32_t total, dyn;
+    asm("mov.u32 %0, %%total_smem_size;" : "=r"(total));
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+    if (addr + width > total + 1024u || width == 0) {
+        printf("ts debug: shared load out of range addr=%u width=%u total=%u dyn=%u\n", addr,
+               width, total, dyn);
+        __trap();
+    }
+}
+#define TS_DBG(addr, w) dbg_check((addr), (w))
+#else
+#define TS_DBG(addr, w) ((void)0)
+#endif
+
 __device__ __forceinline__ uint2 lds64(uint32_t addr) {
+    TS_DBG(addr, 8);
     uint2 v;
     asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
     return v;
 }
 __device__ __forceinline__ float ldsf(uint32_t addr) {
+    TS_DBG(addr, 4);
     float v;
     asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
     return v;
 }
 
 __device__ __forceinline__ uint32_t ldsu(uint32_t addr, int fw) {
+    TS_DBG(addr, fw);
     uint32_t v;
     if (fw == 1) asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
     else asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(addr));
