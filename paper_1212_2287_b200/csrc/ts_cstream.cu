@@ -93,8 +93,11 @@ __device__ __forceinline__ void stage_rows_c(const CStreamArgs &a, float *xs, lo
     if (bad && a.status) atomicOr(a.status, 1);
 }
 
-template <int kK, bool UNIT_W, bool ORD>
+template <int kK, int G, bool UNIT_W, bool ORD>
 __global__ void __launch_bounds__(kThreadsC, 1) k_cstream(CStreamArgs a) {
+    // G instance groups of 32 (B = 32 * G) is a template parameter so the
+    // accumulator's per-lane instance loop is fully unrolled with exactly G
+    // independent f64 chains and the walkers' x-tile stride is an immediate.
     extern __shared__ __align__(128) unsigned char smem[];
     float *xs = reinterpret_cast<float *>(smem);
     float *lb0 = reinterpret_cast<float *>(smem + a.xs_bytes);  // two leaf buffers
@@ -117,7 +120,7 @@ __global__ void __launch_bounds__(kThreadsC, 1) k_cstream(CStreamArgs a) {
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    const int B = a.B;
+    constexpr int B = 32 * G;
     const long long ntiles = (a.n + B - 1) / B;
     const uint32_t lb_half = a.lb_bytes / 2;
 
@@ -142,15 +145,14 @@ __global__ void __launch_bounds__(kThreadsC, 1) k_cstream(CStreamArgs a) {
     }
 
     if (warp == kWarps) {  // ---- accumulator: folds leaves in TREE order
-        const int G = B >> 5;
         uint32_t it = 0;
         for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
             const long long row0 = tile * B;
-            double acc[8];
+            double acc[G];
 #pragma unroll
-            for (int g = 0; g < 8; g++) {
+            for (int g = 0; g < G; g++) {
                 const long long row = row0 + g * 32 + lane;
-                acc[g] = (g < G && a.accumulate && row < a.n) ? a.out[row] : 0.0;
+                acc[g] = (a.accumulate && row < a.n) ? a.out[row] : 0.0;
             }
             for (int c = 0; c < a.nchunks; c++, it++) {
                 const uint4 ci = __ldg(a.chunk_info + a.chunk0 + c);
@@ -163,34 +165,30 @@ __global__ void __launch_bounds__(kThreadsC, 1) k_cstream(CStreamArgs a) {
                     double w = 1.0;
                     if constexpr (!UNIT_W) w = __ldg(a.weight + ci.w + i);
 #pragma unroll
-                    for (int g = 0; g < 8; g++) {
-                        if (g < G) {
-                            const double lv = (double)lbc[i * B + g * 32 + lane];
-                            acc[g] = UNIT_W ? __dadd_rn(acc[g], lv)
-                                            : __dadd_rn(acc[g], __dmul_rn(w, lv));
-                        }
+                    for (int g = 0; g < G; g++) {
+                        const double lv = (double)lbc[i * B + g * 32 + lane];
+                        acc[g] = UNIT_W ? __dadd_rn(acc[g], lv) : __dadd_rn(acc[g], __dmul_rn(w, lv));
                     }
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(lbe + b);
             }
 #pragma unroll
-            for (int g = 0; g < 8; g++) {
+            for (int g = 0; g < G; g++) {
                 const long long row = row0 + g * 32 + lane;
-                if (g < G && row < a.n) a.out[row] = acc[g];
+                if (row < a.n) a.out[row] = acc[g];
             }
         }
         return;
     }
 
     // ---- walkers (8 warps)
-    const int G = B >> 5;
     const int grp = warp % G;
     const int S = kWarps / G;
     const int sub = warp / G;
     const int inst = grp * 32 + lane;
     const uint32_t xr = su32(xs) + 4u * inst;
-    const uint32_t B4 = 4u * B;
+    constexpr uint32_t B4 = 4u * B;
     const uint32_t lbase0 = su32(lb0);
     uint32_t it = 0;
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -305,13 +303,21 @@ bool plan_cstream(int F, int device, CStreamArgs *a) {
 cudaError_t launch_cstream(const CStreamArgs &a, int device, cudaStream_t stream) {
     using namespace cstream_detail;
     if (a.n <= 0) return cudaSuccess;
-    auto pick = [&](auto kk) {
-        constexpr int K = decltype(kk)::value;
-        return a.ord ? (a.unit_w ? k_cstream<K, true, true> : k_cstream<K, false, true>)
-                     : (a.unit_w ? k_cstream<K, true, false> : k_cstream<K, false, false>);
+    auto pick = [&](auto kk, auto gg) {
+        constexpr int K = decltype(kk)::value, G = decltype(gg)::value;
+        return a.ord ? (a.unit_w ? k_cstream<K, G, true, true> : k_cstream<K, G, false, true>)
+                     : (a.unit_w ? k_cstream<K, G, true, false> : k_cstream<K, G, false, false>);
     };
-    auto kern = a.k == 8 ? pick(std::integral_constant<int, 8>{})
-                         : pick(std::integral_constant<int, 4>{});
+    auto pick_g = [&](auto kk) {
+        switch (a.B) {
+            case 256: return pick(kk, std::integral_constant<int, 8>{});
+            case 128: return pick(kk, std::integral_constant<int, 4>{});
+            case 64: return pick(kk, std::integral_constant<int, 2>{});
+            default: return pick(kk, std::integral_constant<int, 1>{});
+        }
+    };
+    auto kern = a.k == 8 ? pick_g(std::integral_constant<int, 8>{})
+                         : pick_g(std::integral_constant<int, 4>{});
     int sms = 0;
     cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     if (e != cudaSuccess) return e;
