@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <atomic>
 #include <string>
+#include <unordered_map>
 
 #include "ts_internal.h"
 
@@ -34,6 +35,33 @@ int cuda_fail(cudaError_t err, const char *what) {
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 int kernel_path() { return g_force_l1; }
+
+const DevAttrs &dev_attrs(int device) {
+    static DevAttrs cache[64];
+    static std::once_flag once[64];
+    if (device < 0 || device >= 64) device = 0;
+    std::call_once(once[device], [device] {
+        cudaDeviceGetAttribute(&cache[device].sms, cudaDevAttrMultiProcessorCount, device);
+        cudaDeviceGetAttribute(&cache[device].smem_optin,
+                               cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    });
+    return cache[device];
+}
+
+cudaError_t ensure_smem(const void *kernel, size_t bytes) {
+    static std::mutex mu;
+    static std::unordered_map<const void *, size_t> granted[64];  // per device
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = granted[dev].find(kernel);
+    if (it != granted[dev].end() && it->second >= bytes) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)bytes);
+    if (e == cudaSuccess) granted[dev][kernel] = bytes;
+    return e;
+}
 
 void free_tables(DeviceTables *t);
 

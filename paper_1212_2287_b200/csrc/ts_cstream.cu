@@ -270,10 +270,8 @@ __global__ void __launch_bounds__(kThreadsC, 1) k_cstream(CStreamArgs a) {
 
 bool plan_cstream(int F, int device, CStreamArgs *a) {
     using namespace cstream_detail;
-    int optin = 0;
-    if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device) !=
-        cudaSuccess)
-        return false;
+    const int optin = dev_attrs(device).smem_optin;
+    if (!optin) return false;
     // Largest instance tile first; then the chain count K whose full round of
     // S * K trees (one K-group per warp) fits a ring stage at ~1.2 KB/tree.
     for (int G = 8; G >= 1; G >>= 1) {
@@ -318,11 +316,10 @@ cudaError_t launch_cstream(const CStreamArgs &a, int device, cudaStream_t stream
     };
     auto kern = a.k == 8 ? pick_g(std::integral_constant<int, 8>{})
                          : pick_g(std::integral_constant<int, 4>{});
-    int sms = 0;
-    cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    if (e != cudaSuccess) return e;
+    const int sms = dev_attrs(device).sms;
+    cudaError_t e;
     const size_t smem = (size_t)a.xs_bytes + a.lb_bytes + (size_t)kStagesC * a.stage_bytes + 8 * 8;
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    e = ensure_smem((const void *)kern, smem);
     if (e != cudaSuccess) return e;
     const long long tiles = (a.n + a.B - 1) / a.B;
     const int grid = (int)(tiles < sms ? tiles : sms);

@@ -143,7 +143,7 @@ struct ScoreArgs {
 // Arguments of the shared-memory streaming kernel (ts_stream.cu).
 constexpr int kStreamMaxDepth = 12;
 struct StreamArgs {
-    int cw;                        // consumer warps per CTA (4: 2 CTAs/SM, 8: 1)
+    int cw;                        // consumer warps per CTA (1: 8 CTAs/SM, 4: 2, 8: 1)
     int fw;                        // deep fid width in bytes (1: F <= 256, else 2)
     const float *x;
     long long n, ld;
@@ -164,7 +164,8 @@ struct StreamArgs {
     long long ld_ord;
     int32_t *status;
 };
-bool plan_stream(int F, int D, int device, StreamArgs *a);
+// n: rows of the launch (-1 at pack time: shape-independent checks only).
+bool plan_stream(int F, int D, int device, StreamArgs *a, long long n = -1);
 inline int split_fid_width(int F) { return F <= 256 ? 1 : 2; }
 cudaError_t launch_stream(int D, const StreamArgs &a, int device, cudaStream_t stream);
 
@@ -199,6 +200,18 @@ cudaError_t launch_segment(const Segment &seg, const ScoreArgs &args, int device
                            cudaStream_t stream);
 
 void count_launch();
+
+// Cached per-device attributes (queried once; cudaDeviceGetAttribute per
+// launch is measurable for small batches).
+struct DevAttrs {
+    int sms = 0;
+    int smem_optin = 0;
+};
+const DevAttrs &dev_attrs(int device);
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) only when a kernel needs
+// more than it was last granted.
+cudaError_t ensure_smem(const void *kernel, size_t bytes);
 int kernel_path();  // ts_set_kernel_path value (0 auto, 1 L1-only)
 
 }  // namespace ts

@@ -238,11 +238,10 @@ __global__ void __launch_bounds__(kMaxWarps * 32, 1) k_compact(ScoreArgs a) {
 template <typename Kern>
 cudaError_t launch(Kern kern, const ScoreArgs &a, int device, size_t smem, int threads,
                    cudaStream_t stream) {
-    int sms = 0;
-    cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    if (e != cudaSuccess) return e;
+    const int sms = dev_attrs(device).sms;
+    cudaError_t e;
     if (smem > 48 * 1024) {
-        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        e = ensure_smem((const void *)kern, smem);
         if (e != cudaSuccess) return e;
     }
     const long long tiles = (a.n + threads - 1) / threads;
@@ -296,7 +295,7 @@ cudaError_t launch_segment(const Segment &seg, const ScoreArgs &args, int device
     }
     if (seg.layout == kSplit) {
         StreamArgs sa{};
-        if (plan_stream(args.F, seg.depth, device, &sa)) {
+        if (plan_stream(args.F, seg.depth, device, &sa, args.n)) {
             sa.x = args.x;
             sa.n = args.n;
             sa.ld = args.ld;
@@ -316,9 +315,7 @@ cudaError_t launch_segment(const Segment &seg, const ScoreArgs &args, int device
         }
         return cudaErrorInvalidConfiguration;  // packed for a device it does not fit
     }
-    int optin = 0;
-    cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
-    if (e != cudaSuccess) return e;
+    const int optin = dev_attrs(device).smem_optin;
     const int rows_per_feature = args.F + (seg.layout == kCompact ? 1 : 0);
     const size_t warp_bytes = (size_t)32 * rows_per_feature * sizeof(float);
     int warps = (int)(optin / warp_bytes);

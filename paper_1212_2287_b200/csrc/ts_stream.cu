@@ -64,7 +64,7 @@ namespace {
 bool plan_stream_cw(int F, int D, int optin, int cw, StreamArgs *a) {
     using namespace stream_detail;
     const int B = 32 * cw;
-    const int ctas = 256 / B;
+    const int ctas = std::min(256 / B, 8);
     // per-CTA budget when several CTAs share an SM (1 KB reserved per CTA)
     if (ctas > 1) optin = std::min(optin, 228 * 1024 / ctas - 1024);
     const size_t xs = ((size_t)F * B * sizeof(float) + 127) & ~(size_t)127;
@@ -88,7 +88,7 @@ bool plan_stream_cw(int F, int D, int optin, int cw, StreamArgs *a) {
         tpc = (uint32_t)(g * K);
     }
     if (!stages) {
-        if (cw == 4) return false;  // the 256-row shape handles it better
+        if (cw != 8) return false;  // the 256-row shape handles it better
         stages = 2;                 // not even two K-groups fit: single trees
         tpc = (uint32_t)std::max<size_t>(1, (ring / 2) / tb);
     }
@@ -104,12 +104,12 @@ bool plan_stream_cw(int F, int D, int optin, int cw, StreamArgs *a) {
 // Shared-memory plan for a segment of depth D over F features: two 128-row
 // CTAs per SM when a full ring of K-groups fits (d <= 9), else one 256-row
 // CTA; false when not even that fits (the caller uses the L1 kernel).
-bool plan_stream(int F, int D, int device, StreamArgs *a) {
+bool plan_stream(int F, int D, int device, StreamArgs *a, long long n) {
     if (D > kStreamMaxDepth) return false;
-    int optin = 0;
-    if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device) !=
-        cudaSuccess)
-        return false;
+    const int optin = dev_attrs(device).smem_optin, sms = dev_attrs(device).sms;
+    if (!optin || !sms) return false;
+    // small batches: 32-row tiles so every SM gets work (layout is identical)
+    if (n >= 0 && n < 2LL * sms * 128 && D <= 8 && plan_stream_cw(F, D, optin, 1, a)) return true;
     if (D <= 9 && plan_stream_cw(F, D, optin, 4, a)) return true;
     return plan_stream_cw(F, D, optin, 8, a);
 }

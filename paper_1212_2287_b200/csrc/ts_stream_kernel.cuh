@@ -37,16 +37,18 @@ namespace stream_detail {
 // CTA shape: CW consumer warps own a tile of B = 32*CW instances, plus one
 // producer warp.  CW = 8: one 256-row CTA per SM; CW = 4: two 128-row CTAs
 // per SM, so one CTA's x staging overlaps the other's walks (used when the
-// trees are small enough for the halved ring, d <= 9).
+// trees are small enough for the halved ring, d <= 9); CW = 1: eight 32-row
+// CTAs per SM for small batches (BASELINE config 0: 10k rows would fill only
+// half the SMs with 128-row tiles).
 template <int CW>
 struct Shape {
     static constexpr int kConsumerWarps = CW;
     static constexpr int kB = CW * 32;
     static constexpr int kThreads = kB + 32;
-    static constexpr int kCtasPerSm = 256 / kB;
+    static constexpr int kCtasPerSm = kB >= 64 ? 256 / kB : 8;
     // Top-level records hold fid << kFidShift = byte offset in a 256-row
-    // x tile; a 128-row tile halves it.
-    static constexpr int kXShift = kB == 256 ? 0 : 1;
+    // x tile; smaller tiles shift it down.
+    static constexpr int kXShift = kB == 256 ? 0 : kB == 128 ? 1 : kB == 64 ? 2 : 3;
 };
 constexpr int kB = 256;  // the irregular-tree kernel's consumer count (ts_cstream.cu)
 constexpr int kMaxStages = 4;
@@ -348,11 +350,10 @@ cudaError_t launch_dc(const StreamArgs &a, int device, cudaStream_t stream) {
     constexpr int kCtasPerSm = Shape<CW>::kCtasPerSm;
     constexpr int kThreads = Shape<CW>::kThreads;
     auto kern = a.fw == 1 ? pick_kernel<D, 1, CW>(a) : pick_kernel<D, 2, CW>(a);
-    int sms = 0;
-    cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    if (e != cudaSuccess) return e;
+    const int sms = dev_attrs(device).sms;
+    cudaError_t e;
     const size_t smem = a.xs_bytes + (size_t)a.stages * a.chunk_cap + 2 * kMaxStages * 8;
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    e = ensure_smem((const void *)kern, smem);
     if (e != cudaSuccess) return e;
     const long long tiles = (a.n + kB - 1) / kB;
     const int grid = (int)(tiles < (long long)sms * kCtasPerSm ? tiles : (long long)sms * kCtasPerSm);
@@ -363,6 +364,8 @@ cudaError_t launch_dc(const StreamArgs &a, int device, cudaStream_t stream) {
 
 template <int D>
 cudaError_t launch_d(const StreamArgs &a, int device, cudaStream_t stream) {
+    if constexpr (D <= 8)
+        if (a.cw == 1) return launch_dc<D, 1>(a, device, stream);
     return a.cw == 4 ? launch_dc<D, 4>(a, device, stream) : launch_dc<D, 8>(a, device, stream);
 }
 
