@@ -37,15 +37,14 @@ namespace stream_detail {
 // CTA shape: CW consumer warps own a tile of B = 32*CW instances, plus one
 // producer warp.  CW = 8: one 256-row CTA per SM; CW = 4: two 128-row CTAs
 // per SM, so one CTA's x staging overlaps the other's walks (used when the
-// trees are small enough for the halved ring, d <= 9); CW = 1: eight 32-row
-// CTAs per SM for small batches (BASELINE config 0: 10k rows would fill only
-// half the SMs with 128-row tiles).
+// trees are small enough for the halved ring, d <= 9).  (Four 32-row CTAs
+// per SM for small batches were tried for config 0 and measured slower.)
 template <int CW>
 struct Shape {
     static constexpr int kConsumerWarps = CW;
     static constexpr int kB = CW * 32;
     static constexpr int kThreads = kB + 32;
-    static constexpr int kCtasPerSm = kB >= 64 ? 256 / kB : 8;
+    static constexpr int kCtasPerSm = kB >= 64 ? 256 / kB : 4;
     // Top-level records hold fid << kFidShift = byte offset in a 256-row
     // x tile; smaller tiles shift it down.
     static constexpr int kXShift = kB == 256 ? 0 : kB == 128 ? 1 : kB == 64 ? 2 : 3;
@@ -364,8 +363,6 @@ cudaError_t launch_dc(const StreamArgs &a, int device, cudaStream_t stream) {
 
 template <int D>
 cudaError_t launch_d(const StreamArgs &a, int device, cudaStream_t stream) {
-    if constexpr (D <= 8)
-        if (a.cw == 1) return launch_dc<D, 1>(a, device, stream);
     return a.cw == 4 ? launch_dc<D, 4>(a, device, stream) : launch_dc<D, 8>(a, device, stream);
 }
 
