@@ -265,7 +265,7 @@ def run_ours(args):
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "roofline_traffic.json")) as fh:
-            traffic = json.load(fh).get("dram_bytes_per_launch")
+            traffic = json.load(fh).get("dram_bytes_per_launch")  # ncu --set full capture
     except Exception:  # noqa: BLE001
         pass
     roofline = {
