@@ -26,6 +26,8 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "ts_internal.h"
@@ -64,7 +66,8 @@ namespace {
 bool plan_stream_cw(int F, int D, int optin, int cw, StreamArgs *a) {
     using namespace stream_detail;
     const int B = 32 * cw;
-    const int ctas = std::min(256 / B, 4);
+    int ctas = std::min(256 / B, 4);
+    if (const char *fc = getenv("TS_STREAM_CTAS")) ctas = std::max(1, std::min(ctas, atoi(fc)));
     // per-CTA budget when several CTAs share an SM (1 KB reserved per CTA)
     if (ctas > 1) optin = std::min(optin, 228 * 1024 / ctas - 1024);
     const size_t xs = ((size_t)F * B * sizeof(float) + 127) & ~(size_t)127;
@@ -109,6 +112,10 @@ bool plan_stream(int F, int D, int device, StreamArgs *a, long long n) {
     const int optin = dev_attrs(device).smem_optin, sms = dev_attrs(device).sms;
     if (!optin || !sms) return false;
     (void)n;  // 32-row tiles for small batches measured slower (cfg0: 17.4 vs 15.2 us)
+    if (const char *fc = getenv("TS_STREAM_CW")) {  // tuning experiments only
+        const int cw = atoi(fc);
+        if ((cw == 4 || cw == 8) && plan_stream_cw(F, D, optin, cw, a)) return true;
+    }
     if (D <= 9 && plan_stream_cw(F, D, optin, 4, a)) return true;
     return plan_stream_cw(F, D, optin, 8, a);
 }
