@@ -16,7 +16,7 @@ namespace ts {
 
 static thread_local std::string g_err;
 static std::atomic<long long> g_launches{0};
-static int g_force_l1 = 0;
+static int g_kernel_path = 0;  // ts_set_kernel_path
 
 void set_error(const std::string &msg) { g_err = msg; }
 
@@ -34,7 +34,7 @@ int cuda_fail(cudaError_t err, const char *what) {
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
-int kernel_path() { return g_force_l1; }
+int kernel_path() { return g_kernel_path; }
 
 const DevAttrs &dev_attrs(int device) {
     static DevAttrs cache[64];
@@ -265,6 +265,6 @@ extern "C" const char *ts_version(void) { return "0.1.0 sm_100a"; }
 
 extern "C" int ts_set_kernel_path(int path) {
     if (path < 0 || path > 1) return fail(TS_ERR_INVALID, "path must be 0 (auto) or 1 (L1 only)");
-    g_force_l1 = path;
+    g_kernel_path = path;
     return TS_OK;
 }

@@ -63,7 +63,6 @@ struct DeviceTables {
     // kCStream chunk tables
     uint4 *chunk_info = nullptr;     // {blob off / 16, bytes, trees, first tree}
     uint32_t *slot_meta = nullptr;   // [chunks][kCStreamMaxT] rec_off/8 | depth<<16 | rel<<21
-    unsigned char *slot_inv = nullptr;  // [chunks][kCStreamMaxT] tree rel -> slot
     // TS_PACK_TRACE only
     TraceNode *trace_nodes = nullptr;
     uint32_t *trace_base = nullptr;  // [T] first node of tree t

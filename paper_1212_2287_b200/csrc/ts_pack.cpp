@@ -214,7 +214,6 @@ void free_tables(DeviceTables *t) {
     cudaFree(t->trace_base);
     cudaFree(t->chunk_info);
     cudaFree(t->slot_meta);
-    cudaFree(t->slot_inv);
     *t = DeviceTables{};
 }
 
@@ -337,7 +336,6 @@ extern "C" int ts_pack_ex(const ts_model_desc *d, int device, int flags, ts_mode
     // kernel's lockstep K-groups walk trees of nearly equal depth.
     std::vector<uint4> chunk_info;
     std::vector<uint32_t> slot_meta;
-    std::vector<unsigned char> slot_inv;
     for (Segment &sg : m->segments) {
         if (sg.layout != kCStream) continue;
         sg.chunk0 = (int)chunk_info.size();
@@ -355,13 +353,11 @@ extern "C" int ts_pack_ex(const ts_model_desc *d, int device, int flags, ts_mode
             });
             const size_t base = slot_meta.size();
             slot_meta.resize(base + kCStreamMaxT, 0u);
-            slot_inv.resize(base + kCStreamMaxT, 0);
             for (int sl = 0; sl < nt; sl++) {
                 const int rel = order[sl];
                 const uint32_t rec8 = (uint32_t)((off[t + rel] - off[t]) / 8);
                 slot_meta[base + sl] = rec8 | ((uint32_t)shapes[t + rel].depth << 16) |
                                        ((uint32_t)rel << 21);
-                slot_inv[base + rel] = (unsigned char)sl;
             }
             t = e;
         }
@@ -380,7 +376,6 @@ extern "C" int ts_pack_ex(const ts_model_desc *d, int device, int flags, ts_mode
     if (!rc) rc = upload(&m->dev.weight, weight);
     if (!rc) rc = upload(&m->dev.chunk_info, chunk_info);
     if (!rc) rc = upload(&m->dev.slot_meta, slot_meta);
-    if (!rc) rc = upload(&m->dev.slot_inv, slot_inv);
     if (!rc && (flags & TS_PACK_TRACE)) {
         // logical trees for the tracer: file-order nodes, leaf ordinals left-to-right
         std::vector<TraceNode> tn(d->tree_node_offset[T]);

@@ -1,31 +1,16 @@
-// ts_stream.cu -- the main sm_100a traversal kernel: complete trees whose
-// node tables are STREAMED through shared memory by the TMA bulk-copy engine.
+// ts_stream.cu -- planning and dispatch for the complete-tree streaming
+// kernel (ts_stream_kernel.cuh; instantiated per depth in ts_stream_i*.cu so
+// nvcc compiles them in parallel).
 //
-// Per CTA (one per SM, persistent over instance tiles):
-//   * 8 consumer warps own a tile of B = 256 instances, staged from HBM and
-//     transposed to xs[f * B + r] (feature-major: lane r's x[fid] reads are
-//     bank-conflict-free for any mix of fids);
-//   * 1 producer warp streams the segment's packed trees, chunk by chunk, into
-//     an S-stage shared-memory ring with cp.async.bulk (TMA, UBLKCP in SASS);
-//     full/empty mbarriers hand stages between producer and consumers, so the
-//     next chunk (and the next tile's first chunks) land while the current
-//     one is walked;
-//   * each consumer thread walks K trees of the chunk at once (K independent
-//     index chains for latency hiding): per level
-//         rec = node[j] (LDS.64 {fid, theta});  v = xs[fid*B + r] (LDS);
-//         j = 2j + 1 + (v >= theta)
-//     -- the reference's update i = (i<<1)+1+(x[fid[i]] >= theta[i])
-//     (ref evaluators.py:90-99) -- then adds w*leaf in f64, tree order
-//     (ref evaluators.py:529-535; __dmul_rn/__dadd_rn, never an FMA).
-//
-// Chunk = `tpc` consecutive trees of one complete segment (all of depth D,
-// so every tree record has the same size and chunk c starts at
-// c * tpc * tree_bytes).  Tree record: (2^D - 1) uint2 {fid, theta bits} in
-// heap order, then 2^D fp32 leaves, padded to 16 bytes.
+// plan_stream() sizes one CTA: x tile (B rows x F features, fp32,
+// feature-major) + a ring of 2-4 stages, each holding a whole number of
+// K-groups of kSplit tree records; it prefers two 128-row CTAs per SM
+// (d <= 9) so one CTA's x staging overlaps the other's walks, and one 256-row
+// CTA otherwise.  Trees that do not fit (d > 12 or rows too wide) fall back to
+// the L1-path kernels in ts_kernels.cu.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
-
 #include <stdlib.h>
 
 #include <algorithm>

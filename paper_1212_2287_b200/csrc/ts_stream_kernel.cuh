@@ -1,28 +1,30 @@
 #pragma once
-// ts_stream.cu -- the main sm_100a traversal kernel: complete trees whose
-// node tables are STREAMED through shared memory by the TMA bulk-copy engine.
+// ts_stream_kernel.cuh -- the main sm_100a traversal kernel: complete trees
+// whose node tables are STREAMED through shared memory by the TMA bulk-copy
+// engine (planning/dispatch: ts_stream.cu).
 //
-// Per CTA (one per SM, persistent over instance tiles):
-//   * 8 consumer warps own a tile of B = 256 instances, staged from HBM and
-//     transposed to xs[f * B + r] (feature-major: lane r's x[fid] reads are
-//     bank-conflict-free for any mix of fids);
+// Per CTA (persistent over instance tiles; 1 or 2 per SM, see Shape):
+//   * CW consumer warps own a tile of B = 32*CW instances, staged from HBM
+//     and transposed to xs[f * B + r] (feature-major: lane r's x[fid] reads
+//     are bank-conflict-free for any mix of fids);
 //   * 1 producer warp streams the segment's packed trees, chunk by chunk, into
-//     an S-stage shared-memory ring with cp.async.bulk (TMA, UBLKCP in SASS);
+//     a 2-4 stage shared-memory ring with cp.async.bulk (TMA, UBLKCP in SASS);
 //     full/empty mbarriers hand stages between producer and consumers, so the
 //     next chunk (and the next tile's first chunks) land while the current
 //     one is walked;
-//   * each consumer thread walks K trees of the chunk at once (K independent
-//     index chains for latency hiding): per level
-//         rec = node[j] (LDS.64 {fid, theta});  v = xs[fid*B + r] (LDS);
-//         j = 2j + 1 + (v >= theta)
+//   * each consumer thread walks K trees of the chunk in lockstep (K
+//     independent chains for latency hiding), level by level:
+//         top levels (< kTopLevels): rec = {fid << 10, theta} (LDS.64),
+//           v = xs[fid][r] (LDS), heap step j -> 2j + 1 + (v >= theta)
+//         deep levels: theta (LDS.32) and fid (LDS.U8/U16) from per-level
+//           arrays, same predicate
 //     -- the reference's update i = (i<<1)+1+(x[fid[i]] >= theta[i])
 //     (ref evaluators.py:90-99) -- then adds w*leaf in f64, tree order
 //     (ref evaluators.py:529-535; __dmul_rn/__dadd_rn, never an FMA).
 //
 // Chunk = `tpc` consecutive trees of one complete segment (all of depth D,
 // so every tree record has the same size and chunk c starts at
-// c * tpc * tree_bytes).  Tree record: (2^D - 1) uint2 {fid, theta bits} in
-// heap order, then 2^D fp32 leaves, padded to 16 bytes.
+// c * tpc * tree_bytes).  Record layout: kSplit / split_geom (ts_internal.h).
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
