@@ -179,7 +179,6 @@ struct CStreamArgs {
     const unsigned char *blob;
     const uint4 *chunk_info;
     const uint32_t *slot_meta;
-    const unsigned char *slot_inv;
     int chunk0, nchunks;
     int tpc;               // max trees per chunk
     int k;                 // lockstep chains per thread (4 or 8)

@@ -281,7 +281,6 @@ cudaError_t launch_segment(const Segment &seg, const ScoreArgs &args, int device
         ca.blob = args.blob;
         ca.chunk_info = args.tables->chunk_info;
         ca.slot_meta = args.tables->slot_meta;
-        ca.slot_inv = args.tables->slot_inv;
         ca.chunk0 = seg.chunk0;
         ca.nchunks = seg.nchunks;
         ca.weight = args.weight;
