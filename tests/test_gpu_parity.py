@@ -236,3 +236,78 @@ def test_predict_fvec_streams_files(tmp_path):
     write_fvec(path, X)
     with pytest.raises(ValueError, match="non-finite"):
         ev.predict_fvec(path, chunk_rows=128)
+
+
+@pytest.mark.parametrize("depth", [13, 16])
+def test_deep_complete_trees_l1_path(depth):
+    # complete trees deeper than the streaming kernel handles (d > 12) run on
+    # the L1-path heap kernel
+    from paper_1212_2287_b200 import synth
+    rng = np.random.default_rng(depth)
+    T, F = 3, 20
+    n_int = (1 << depth) - 1
+    flat = synth.complete_flat(F, depth, rng.integers(0, F, (T, n_int)),
+                               rng.random((T, n_int), dtype=np.float32),
+                               rng.standard_normal((T, 1 << depth)).astype(np.float32),
+                               weights=[0.5, 1.0, -2.0])
+    X = rng.random((777, F), dtype=np.float32)
+    ev = _ev(flat)
+    c = oracle.COracle(flat.arrays())
+    ref, ref_ord = c.score(X, with_ordinals=True)
+    assert np.array_equal(ev.predict_batch(X), ref)
+    assert np.array_equal(ev.leaf_indices(X), ref_ord.astype(np.int64))
+
+
+def test_tiny_shapes_and_padded_ordinals():
+    import torch
+    from paper_1212_2287_b200 import Ensemble, Node, Tree
+    ens = Ensemble(1, [Tree(Node.internal(0, 0.25, Node.leaf(-1.5), Node.leaf(2.5))),
+                       (Tree(Node.leaf(0.125)), 3.0)])
+    ev = _ev(ens)
+    assert ev.predict(np.array([0.25], np.float32)) == 2.5 + 3.0 * 0.125
+    x = torch.tensor([[0.0], [0.3]], dtype=torch.float32, device="cuda")
+    ords = torch.full((2, 64), -1, dtype=torch.int16, device="cuda")   # ld_ord > n
+    ev.model.score(x, ordinals=ords)
+    torch.cuda.synchronize()
+    o = ords.cpu().numpy()
+    assert o[:, :2].tolist() == [[0, 1], [0, 0]] and (o[:, 2:] == -1).all()
+
+
+def test_models_on_concurrent_streams():
+    import torch
+    w1 = __import__("paper_1212_2287_b200").synth.config2(6, n=5000, trees=64)
+    ens, g = load_golden("mixed")
+    ev1, ev2 = _ev(w1.flat), _ev(ens)
+    x1 = torch.from_numpy(w1.x).cuda()
+    x2 = torch.from_numpy(g["X"]).cuda()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    outs = []
+    for _ in range(3):
+        with torch.cuda.stream(s1):
+            o1 = ev1.score_device(x1, stream=s1)
+        with torch.cuda.stream(s2):
+            o2 = ev2.score_device(x2, stream=s2)
+        outs.append((o1, o2))
+    torch.cuda.synchronize()
+    ref1 = oracle.COracle(w1.flat.arrays()).score(w1.x)
+    for o1, o2 in outs:
+        assert np.array_equal(o1.cpu().numpy(), ref1)
+        assert np.array_equal(o2.cpu().numpy(), g["scores"])
+
+
+def test_invalid_models_rejected_by_packer():
+    from paper_1212_2287_b200 import FlatModel, GpuModel, ModelSemanticError
+    bad = [
+        FlatModel(2, np.array([0, 3]), np.array([1.0]), np.array([0, -1, -1], np.int32),
+                  np.array([0.5, 1, 2], np.float32), np.array([1, -1, -1], np.int32),
+                  np.array([1, -1, -1], np.int32)),                    # two parents
+        FlatModel(2, np.array([0, 3]), np.array([np.nan]), np.array([0, -1, -1], np.int32),
+                  np.array([0.5, 1, 2], np.float32), np.array([1, -1, -1], np.int32),
+                  np.array([2, -1, -1], np.int32)),                    # NaN weight
+        FlatModel(2, np.array([0, 3]), np.array([1.0]), np.array([0, -1, -1], np.int32),
+                  np.array([0.5, 1, 2], np.float32), np.array([1, -1, -1], np.int32),
+                  np.array([0, -1, -1], np.int32)),                    # root as child
+    ]
+    for fm in bad:
+        with pytest.raises(ModelSemanticError):
+            GpuModel(fm)
