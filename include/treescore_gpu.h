@@ -133,6 +133,41 @@ int ts_trace(const ts_model *model, const float *x, int64_t n, int64_t f, int64_
              double *out, uint16_t *leaf_ord, int64_t ld_ord, uint32_t *visited,
              int32_t words, void *stream);
 
+/* Fused cross-GPU running-sum pipeline for TREE-SHARDED scoring (BASELINE
+ * config 4b), bit-exact: rank r holds trees [t_r, t_{r+1}) and scores all n
+ * rows; inside the kernel each 32-row block waits until flags_in[block] ==
+ * epoch (set by rank r-1 over NVLink, system-scope acquire), continues the f64
+ * sums from sums_in, and when its walk over rank r's trees is done stores the
+ * running sums straight into rank r+1's sums_in (a peer pointer from
+ * ts_ipc_open) and releases flags_out[block] = epoch.  Transfers overlap the
+ * walks block by block; every addition happens in global tree order, so the
+ * last rank's `out` equals single-GPU scoring bit for bit.
+ *   sums_in / flags_in   NULL on the first rank (start at +0.0)
+ *   sums_out / flags_out NULL on the last rank (write `out`)
+ *   epoch                increases by one per call (flags are never reset)
+ * Needs a model packed as one streaming segment of complete trees
+ * (TS_ERR_UNSUPPORTED otherwise).  Calls must be separated by a host barrier
+ * across ranks (a rank may not overwrite sums it has not seen consumed). */
+typedef struct {
+    const double *sums_in;
+    const uint32_t *flags_in;
+    double *sums_out;
+    uint32_t *flags_out;
+    uint32_t epoch;
+} ts_pipe;
+
+int ts_score_pipe(const ts_model *model, const float *x, int64_t n, int64_t f, int64_t ld,
+                  double *out, const ts_pipe *pipe, void *stream);
+
+/* Pipeline receive buffers: f64 sums[n] and u32 flags[ceil(n/32)] (zeroed),
+ * as their own cudaMalloc allocations on `device`, with CUDA IPC handles
+ * (64 bytes each) for the previous rank to open with ts_ipc_open. */
+int ts_pipe_alloc(int device, int64_t n, double **sums, uint32_t **flags,
+                  void *sums_handle64, void *flags_handle64);
+void ts_pipe_free(double *sums, uint32_t *flags);
+int ts_ipc_open(const void *handle64, void **dev_ptr);
+void ts_ipc_close(void *dev_ptr);
+
 /* Host-buffer scoring: same argument meaning as the reference's generated
  * score_batch(x, n, f, out).  Copies x to the device in chunks on two
  * streams (H2D of chunk i+1 overlaps scoring of chunk i), copies the scores

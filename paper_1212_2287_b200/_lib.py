@@ -29,7 +29,8 @@ TS_PACK_TRACE = 1
 # Every symbol include/treescore_gpu.h declares (checked by the CPU tests).
 EXPORTS = ("ts_pack", "ts_pack_ex", "ts_trace", "ts_model_get_info", "ts_score", "ts_score_ex", "ts_score_host", "ts_free",
            "ts_last_error", "ts_launch_count", "ts_version", "ts_synth_uniform", "ts_set_kernel_path",
-           "ts_parse_model", "ts_flat_free")
+           "ts_parse_model", "ts_flat_free", "ts_score_pipe", "ts_pipe_alloc", "ts_pipe_free",
+           "ts_ipc_open", "ts_ipc_close")
 
 
 class NativeLibraryError(RuntimeError):
@@ -59,6 +60,14 @@ class FlatModelC(ctypes.Structure):
                 ("node_right", ctypes.POINTER(ctypes.c_int32)),
                 ("err_line", ctypes.c_int32),
                 ("err_col", ctypes.c_int32)]
+
+
+class Pipe(ctypes.Structure):
+    _fields_ = [("sums_in", ctypes.c_void_p),
+                ("flags_in", ctypes.c_void_p),
+                ("sums_out", ctypes.c_void_p),
+                ("flags_out", ctypes.c_void_p),
+                ("epoch", ctypes.c_uint32)]
 
 
 class ModelInfo(ctypes.Structure):
@@ -132,6 +141,16 @@ def load(build_if_missing: bool = True):
         lib.ts_parse_model.restype = ctypes.c_int
         lib.ts_flat_free.argtypes = [ctypes.POINTER(FlatModelC)]
         lib.ts_flat_free.restype = None
+        lib.ts_score_pipe.argtypes = [P, P, I64, I64, I64, P, ctypes.POINTER(Pipe), P]
+        lib.ts_score_pipe.restype = ctypes.c_int
+        lib.ts_pipe_alloc.argtypes = [ctypes.c_int, I64, ctypes.POINTER(P), ctypes.POINTER(P), P, P]
+        lib.ts_pipe_alloc.restype = ctypes.c_int
+        lib.ts_pipe_free.argtypes = [P, P]
+        lib.ts_pipe_free.restype = None
+        lib.ts_ipc_open.argtypes = [P, ctypes.POINTER(P)]
+        lib.ts_ipc_open.restype = ctypes.c_int
+        lib.ts_ipc_close.argtypes = [P]
+        lib.ts_ipc_close.restype = None
         for name in EXPORTS:
             getattr(lib, name)
         _lib = lib

@@ -83,7 +83,8 @@ struct DeviceGuard {
 
 int score_device(const ts_model *m, const float *x, int64_t n, int64_t f, int64_t ld,
                  double *out, uint16_t *ord, int64_t ld_ord, int32_t *status,
-                 cudaStream_t stream, bool accumulate = false) {
+                 cudaStream_t stream, bool accumulate = false,
+                 const PipeArgs *pipe = nullptr) {
     if (n == 0) return TS_OK;
     ScoreArgs a{};
     a.x = x;
@@ -107,6 +108,7 @@ int score_device(const ts_model *m, const float *x, int64_t n, int64_t f, int64_
         a.accumulate = accumulate || s > 0;
         // Only the first launch of a call needs to flag non-finite input.
         a.status = s == 0 ? status : nullptr;
+        if (pipe) a.pipe = *pipe;
         cudaError_t e = launch_segment(seg, a, m->device, stream);
         if (e != cudaSuccess) return cuda_fail(e, "scoring kernel launch");
     }
@@ -160,6 +162,74 @@ extern "C" int ts_score_ex(const ts_model *m, const float *x, int64_t n, int64_t
     if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
     return score_device(m, x, n, f, ld, out, ord_out, ld_ord, status, (cudaStream_t)stream,
                         accumulate != 0);
+}
+
+extern "C" int ts_score_pipe(const ts_model *m, const float *x, int64_t n, int64_t f,
+                             int64_t ld, double *out, const ts_pipe *pipe, void *stream) {
+    int rc = check_args(m, x, n, f, ld, out);
+    if (rc) return rc;
+    if (!pipe) return fail(TS_ERR_INVALID, "pipe is NULL");
+    if (m->segments.size() != 1 || m->segments[0].layout != kSplit)
+        return fail(TS_ERR_UNSUPPORTED,
+                    "the fused pipeline needs one streaming segment of complete trees");
+    if ((pipe->sums_in == nullptr) != (pipe->flags_in == nullptr) ||
+        (pipe->sums_out == nullptr) != (pipe->flags_out == nullptr))
+        return fail(TS_ERR_INVALID, "pipe sums and flags must be given together");
+    DeviceGuard g(m->device);
+    if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
+    PipeArgs p;
+    p.sums_in = pipe->sums_in;
+    p.flags_in = pipe->flags_in;
+    p.sums_out = pipe->sums_out;
+    p.flags_out = pipe->flags_out;
+    p.epoch = pipe->epoch;
+    p.nblocks = (n + 31) / 32;
+    return score_device(m, x, n, f, ld, out, nullptr, 0, nullptr, (cudaStream_t)stream, false,
+                        &p);
+}
+
+extern "C" int ts_pipe_alloc(int device, int64_t n, double **sums, uint32_t **flags,
+                             void *sums_handle64, void *flags_handle64) {
+    if (!sums || !flags || n < 1) return fail(TS_ERR_INVALID, "bad pipe allocation request");
+    *sums = nullptr;
+    *flags = nullptr;
+    DeviceGuard g(device);
+    if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
+    const size_t nb = (size_t)(n + 31) / 32;
+    cudaError_t e;
+    if ((e = cudaMalloc(sums, n * sizeof(double))) ||
+        (e = cudaMalloc(flags, nb * sizeof(uint32_t))) ||
+        (e = cudaMemset(*flags, 0, nb * sizeof(uint32_t)))) {
+        cudaFree(*sums);
+        cudaFree(*flags);
+        *sums = nullptr;
+        *flags = nullptr;
+        return cuda_fail(e, "ts_pipe_alloc");
+    }
+    cudaIpcMemHandle_t hs, hf;
+    if (sums_handle64 && (e = cudaIpcGetMemHandle(&hs, *sums)) == cudaSuccess)
+        memcpy(sums_handle64, &hs, sizeof hs);
+    if (e == cudaSuccess && flags_handle64 && (e = cudaIpcGetMemHandle(&hf, *flags)) == cudaSuccess)
+        memcpy(flags_handle64, &hf, sizeof hf);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle");
+    return TS_OK;
+}
+
+extern "C" void ts_pipe_free(double *sums, uint32_t *flags) {
+    cudaFree(sums);
+    cudaFree(flags);
+}
+
+extern "C" int ts_ipc_open(const void *handle64, void **dev_ptr) {
+    if (!handle64 || !dev_ptr) return fail(TS_ERR_INVALID, "NULL argument");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle64, sizeof h);
+    cudaError_t e = cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess);
+    return e == cudaSuccess ? TS_OK : cuda_fail(e, "cudaIpcOpenMemHandle");
+}
+
+extern "C" void ts_ipc_close(void *dev_ptr) {
+    if (dev_ptr) cudaIpcCloseMemHandle(dev_ptr);
 }
 
 extern "C" int ts_score_host(const ts_model *mc, const float *x, int64_t n, int64_t f,

@@ -121,6 +121,16 @@ void set_error(const std::string &msg);
 int fail(int code, const std::string &msg);
 int cuda_fail(cudaError_t err, const char *what);
 
+// Cross-GPU running-sum pipeline of ts_score_pipe (32-row blocks).
+struct PipeArgs {
+    const double *sums_in = nullptr;       // running sums from the previous rank
+    const uint32_t *flags_in = nullptr;    // [nblocks], == epoch when published
+    double *sums_out = nullptr;            // next rank's sums_in (peer pointer)
+    uint32_t *flags_out = nullptr;         // next rank's flags_in (peer pointer)
+    uint32_t epoch = 0;
+    long long nblocks = 0;
+};
+
 struct ScoreArgs {
     const float *x;
     long long n, ld;
@@ -137,6 +147,7 @@ struct ScoreArgs {
     uint16_t *ord;
     long long ld_ord;
     int32_t *status;
+    PipeArgs pipe;  // k_stream only (ts_score_pipe)
 };
 
 // Arguments of the shared-memory streaming kernel (ts_stream.cu).
@@ -162,6 +173,7 @@ struct StreamArgs {
     uint16_t *ord;
     long long ld_ord;
     int32_t *status;
+    PipeArgs pipe;
 };
 // n: rows of the launch (-1 at pack time: shape-independent checks only).
 bool plan_stream(int F, int D, int device, StreamArgs *a, long long n = -1);

@@ -310,6 +310,7 @@ cudaError_t launch_segment(const Segment &seg, const ScoreArgs &args, int device
             sa.ord = args.ord;
             sa.ld_ord = args.ld_ord;
             sa.status = args.status;
+            sa.pipe = args.pipe;
             return launch_stream(seg.depth, sa, device, stream);
         }
         return cudaErrorInvalidConfiguration;  // packed for a device it does not fit

@@ -27,6 +27,7 @@
 // c * tpc * tree_bytes).  Record layout: kSplit / split_geom (ts_internal.h).
 #include <cuda_runtime.h>
 #include <math.h>
+#include <stdio.h>
 #include <stdint.h>
 
 #include <algorithm>
@@ -99,6 +100,35 @@ __device__ __forceinline__ void consumer_sync() {
     asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
 }
 __device__ __forceinline__ bool finite_f(float v) { return fabsf(v) <= 3.402823466e38f; }
+
+// Pipeline flags: system-scope acquire/release, written by one GPU and read
+// by another over NVLink (ts_score_pipe).  A producer that never publishes
+// (its rank died) traps after kPipeTimeoutNs instead of hanging the GPU.
+constexpr unsigned long long kPipeTimeoutNs = 20ull * 1000 * 1000 * 1000;
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void pipe_wait(const uint32_t *flag, uint32_t epoch) {
+    uint32_t v;
+    unsigned long long t0 = 0;
+    while (true) {
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+        if (v == epoch) break;
+        const unsigned long long t = global_ns();
+        if (t0 == 0) t0 = t;
+        else if (t - t0 > kPipeTimeoutNs) {
+            printf("ts_score_pipe: no sums from the previous rank after %llus (flag %u, "
+                   "epoch %u)\n", kPipeTimeoutNs / 1000000000ull, v, epoch);
+            __trap();
+        }
+        __nanosleep(256);
+    }
+}
+__device__ __forceinline__ void pipe_signal(uint32_t *flag, uint32_t epoch) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(epoch) : "memory");
+}
 
 // Transposing stage of B rows into xs[f * B + r] (consumer threads only).
 template <int B>
@@ -317,6 +347,14 @@ __global__ void __launch_bounds__(Shape<CW>::kThreads, Shape<CW>::kCtasPerSm)
         stage_rows<kB>(a, xs, tile * kB);
         consumer_sync<kB>();
         double acc = (a.accumulate && valid) ? a.out[row] : 0.0;
+        // Cross-GPU running-sum pipeline (ts_score_pipe): this warp's 32-row
+        // block continues the sums the previous rank published for it.
+        const long long blk = tile * (long long)CW + warp;
+        if (a.pipe.flags_in) {
+            if (lane == 0 && blk < a.pipe.nblocks) pipe_wait(a.pipe.flags_in + blk, a.pipe.epoch);
+            __syncwarp();
+            acc = valid ? __ldcv(a.pipe.sums_in + row) : 0.0;
+        }
         for (int c = 0; c < nchunks; c++, it++) {
             const int s = it % kStages;
             mbar_wait(full + s, (it / kStages) & 1);
@@ -333,7 +371,15 @@ __global__ void __launch_bounds__(Shape<CW>::kThreads, Shape<CW>::kCtasPerSm)
             __syncwarp();
             if (lane == 0) mbar_arrive(empty + s);
         }
-        if (valid) a.out[row] = acc;
+        if (a.pipe.sums_out) {
+            // publish to the next rank (peer memory over NVLink), then flag
+            if (valid) a.pipe.sums_out[row] = acc;
+            __threadfence_system();
+            __syncwarp();
+            if (lane == 0 && blk < a.pipe.nblocks) pipe_signal(a.pipe.flags_out + blk, a.pipe.epoch);
+        } else if (valid) {
+            a.out[row] = acc;
+        }
     }
 }
 

@@ -19,6 +19,15 @@ SURVEY.md section 8(e): instances are independent, so the path shards two ways.
       NCCL send/recv.  Every addition happens in the reference's tree order,
       so the final scores are bit-identical to single-GPU scoring; the cost is
       (R - 1) chunk times of pipeline fill.
+    - ``"p2p"``: the same bit-exact order, fused into the scoring kernel
+      (``ts_score_pipe``): each 32-row block of rank r waits on a
+      system-scope flag that rank r-1's kernel releases after storing the
+      block's running sums straight into rank r's HBM over NVLink (CUDA IPC
+      peer pointers).  No NCCL and no host round trip on the data path; the
+      transfers overlap the walks block by block.  Needs one process per GPU:
+      the ranks' kernels wait on each other, so they must run concurrently
+      (``serialize=True`` runs the ranks one after another for tests that
+      share one GPU).
 
 The per-rank scorer is injected (``make_scorer``) so the same driver runs on
 GPUs (the CUDA library) and, in the CPU test-suite, under ``gloo`` with the
@@ -65,7 +74,7 @@ def tree_shards(depths, world: int) -> list[tuple[int, int]]:
 
 @dataclass
 class ShardPlan:
-    mode: str                      # "instance" | "tree-reduce" | "tree-pipeline"
+    mode: str                      # "instance" | "tree-reduce" | "tree-pipeline" | "tree-p2p"
     world: int
     rank: int
     rows: tuple[int, int]          # rows this rank scores
@@ -76,7 +85,7 @@ def plan(mode: str, n: int, flat: FlatModel, world: int, rank: int,
          depths=None) -> ShardPlan:
     if mode == "instance":
         return ShardPlan(mode, world, rank, row_shard(n, world, rank), (0, flat.num_trees))
-    if mode in ("tree-reduce", "tree-pipeline"):
+    if mode in ("tree-reduce", "tree-pipeline", "tree-p2p"):
         d = flat.depths() if depths is None else depths
         return ShardPlan(mode, world, rank, (0, n), tree_shards(d, world)[rank])
     raise ValueError(f"unknown shard mode {mode!r}")
@@ -104,21 +113,41 @@ class ShardedScorer:
     all ``n_total`` rows for the tree modes.  ``__call__`` returns the rank's
     row-shard scores for ``"instance"``; for the tree modes the full f64
     ``[n_total]`` scores land on rank 0 (``"tree-reduce"``) or on the last
-    rank (``"tree-pipeline"``), partial sums elsewhere.
+    rank (``"tree-pipeline"``, ``"tree-p2p"``), partial sums elsewhere.
     """
 
     def __init__(self, mode: str, flat: FlatModel, n_total: int, *, group=None,
                  make_scorer: Callable | None = None, device=None, depths=None,
-                 chunk_rows: int = 1 << 17):
+                 chunk_rows: int = 1 << 17, serialize: bool = False):
         import torch.distributed as dist
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         self.n_total = n_total
         self.chunk_rows = chunk_rows
+        self.serialize = serialize
         self.plan = plan(mode, n_total, flat, self.world, self.rank, depths)
         shard = flat if mode == "instance" else flat.subset(*self.plan.trees)
         self.score = (make_scorer or (lambda fm: gpu_scorer(fm, device)))(shard)
+        if mode == "tree-p2p":
+            self._setup_p2p(device)
+
+    def _setup_p2p(self, device):
+        """Allocate this rank's receive buffers, publish their IPC handles and
+        map the next rank's (all_gather_object on the host; once)."""
+        import torch
+        import torch.distributed as dist
+        from .evaluator import PeerBuffers, PipeBuffers
+        model = getattr(self.score, "model", None)
+        if model is None:
+            raise ValueError("tree-p2p needs the CUDA scorer (gpu_scorer)")
+        dev = torch.cuda.current_device() if device is None else int(device)
+        self.recv = PipeBuffers(self.n_total, dev) if self.rank > 0 else None
+        handles = [None] * self.world
+        dist.all_gather_object(handles, self.recv.handles if self.recv else None,
+                               group=self.group)
+        self.send = PeerBuffers(handles[self.rank + 1]) if self.rank < self.world - 1 else None
+        self.epoch = 0
 
     def __call__(self, x_local, out=None):
         import torch
@@ -136,6 +165,8 @@ class ShardedScorer:
             self.score(x_local, out, False)
             dist.reduce(out, dst=0, op=dist.ReduceOp.SUM, group=grp)
             return out
+        if mode == "tree-p2p":
+            return self._call_p2p(x_local, out)
         # tree-pipeline: chunk c visits ranks 0..R-1 in order; rank r receives
         # the running sums of chunk c from r-1, continues them over its trees
         # and sends them on.
@@ -148,6 +179,36 @@ class ShardedScorer:
             if rank < world - 1:
                 dist.send(seg, dst=rank + 1, group=grp)
         return out
+
+
+    def _call_p2p(self, x_local, out):
+        import torch
+        import torch.distributed as dist
+        self.epoch += 1
+        model = self.score.model
+        kw = dict(epoch=self.epoch)
+        if self.recv is not None:
+            kw.update(sums_in=self.recv.sums, flags_in=self.recv.flags)
+        if self.send is not None:
+            kw.update(sums_out=self.send.sums, flags_out=self.send.flags)
+        steps = range(self.world) if self.serialize else (self.rank,)
+        for step in steps:
+            if step == self.rank:
+                model.score_pipe(x_local, out, **kw)
+                torch.cuda.current_stream(x_local.device).synchronize()
+            if self.serialize:
+                dist.barrier(group=self.group)
+        if not self.serialize:
+            # the next call may overwrite the next rank's sums only after it
+            # consumed this call's (flags are per epoch, buffers are not)
+            torch.cuda.current_stream(x_local.device).synchronize()
+            dist.barrier(group=self.group)
+        return out
+
+    def close(self):
+        for b in (getattr(self, "recv", None), getattr(self, "send", None)):
+            if b is not None:
+                b.close()
 
 
 def run_sharded(mode: str, flat: FlatModel, x_local, n_total: int, **kw):

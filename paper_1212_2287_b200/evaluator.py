@@ -148,6 +148,33 @@ class GpuModel:
             raise RuntimeError(f"ts_score failed ({rc}): {_lib.last_error()}")
         return out
 
+    def score_pipe(self, x, out=None, sums_in=0, flags_in=0, sums_out=0, flags_out=0,
+                   epoch=1, stream=None):
+        """``ts_score_pipe``: one stage of the fused cross-GPU running-sum pipeline.
+
+        ``sums_in``/``flags_in``: this rank's :class:`PipeBuffers` (0 on the
+        first rank); ``sums_out``/``flags_out``: the next rank's buffers as
+        device pointers (:class:`PeerBuffers`, 0 on the last rank, which
+        writes ``out``).  ``epoch`` must grow by one per call.
+        """
+        torch = _torch()
+        if x.dim() != 2 or x.dtype != torch.float32 or not x.is_cuda or x.stride(1) != 1:
+            raise TypeError("x must be a row-major 2-D float32 CUDA tensor")
+        n, f = x.shape
+        if out is None:
+            out = torch.empty(n, dtype=torch.float64, device=x.device)
+        if stream is None:
+            stream = torch.cuda.current_stream(x.device)
+        pipe = _lib.Pipe(sums_in or None, flags_in or None, sums_out or None, flags_out or None,
+                         int(epoch) & 0xFFFFFFFF)
+        ld = x.stride(0) if n > 1 else f
+        rc = self._lib.ts_score_pipe(self.handle, ctypes.c_void_p(x.data_ptr()), n, f, ld,
+                                     ctypes.c_void_p(out.data_ptr()), ctypes.byref(pipe),
+                                     ctypes.c_void_p(stream.cuda_stream))
+        if rc != _lib.TS_OK:
+            raise RuntimeError(f"ts_score_pipe failed ({rc}): {_lib.last_error()}")
+        return out
+
     def trace(self, x, out=None, leaf_ord=None, visited=None, stream=None):
         """``ts_trace`` on a CUDA float32 ``[n, f]`` tensor (model packed with trace=True)."""
         torch = _torch()
@@ -178,6 +205,62 @@ class GpuModel:
         if getattr(self, "handle", None) is not None and self.handle.value:
             self._lib.ts_free(self.handle)
             self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 - interpreter shutdown
+            pass
+
+
+class PipeBuffers:
+    """This rank's receive side of the fused pipeline (``ts_pipe_alloc``):
+    f64 ``sums[n]`` and zeroed u32 ``flags[ceil(n/32)]`` plus 64-byte CUDA IPC
+    handles the previous rank opens with :class:`PeerBuffers`."""
+
+    def __init__(self, n: int, device: int):
+        self._lib = lib = _lib.load()
+        s, f = ctypes.c_void_p(), ctypes.c_void_p()
+        hs, hf = ctypes.create_string_buffer(64), ctypes.create_string_buffer(64)
+        rc = lib.ts_pipe_alloc(int(device), int(n), ctypes.byref(s), ctypes.byref(f), hs, hf)
+        if rc != _lib.TS_OK:
+            raise RuntimeError(f"ts_pipe_alloc failed ({rc}): {_lib.last_error()}")
+        self.sums, self.flags = s.value, f.value
+        self.handles = (hs.raw, hf.raw)
+
+    def close(self):
+        if getattr(self, "sums", None):
+            self._lib.ts_pipe_free(self.sums, self.flags)
+            self.sums = self.flags = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 - interpreter shutdown
+            pass
+
+
+class PeerBuffers:
+    """Another process's :class:`PipeBuffers` mapped here (``ts_ipc_open``)."""
+
+    def __init__(self, handles):
+        self._lib = lib = _lib.load()
+        ptrs = []
+        for h in handles:
+            p = ctypes.c_void_p()
+            rc = lib.ts_ipc_open(ctypes.create_string_buffer(bytes(h), 64), ctypes.byref(p))
+            if rc != _lib.TS_OK:
+                for q in ptrs:
+                    lib.ts_ipc_close(q)
+                raise RuntimeError(f"ts_ipc_open failed ({rc}): {_lib.last_error()}")
+            ptrs.append(p.value)
+        self.sums, self.flags = ptrs
+
+    def close(self):
+        if getattr(self, "sums", None):
+            self._lib.ts_ipc_close(self.sums)
+            self._lib.ts_ipc_close(self.flags)
+            self.sums = self.flags = None
 
     def __del__(self):
         try:
