@@ -27,7 +27,6 @@
 // c * tpc * tree_bytes).  Record layout: kSplit / split_geom (ts_internal.h).
 #include <cuda_runtime.h>
 #include <math.h>
-#include <stdio.h>
 #include <stdint.h>
 
 #include <algorithm>
@@ -103,7 +102,8 @@ __device__ __forceinline__ bool finite_f(float v) { return fabsf(v) <= 3.4028234
 
 // Pipeline flags: system-scope acquire/release, written by one GPU and read
 // by another over NVLink (ts_score_pipe).  A producer that never publishes
-// (its rank died) traps after kPipeTimeoutNs instead of hanging the GPU.
+// (its rank died) traps after kPipeTimeoutNs instead of hanging the GPU (the
+// launch then fails with cudaErrorLaunchFailure on the host).
 constexpr unsigned long long kPipeTimeoutNs = 20ull * 1000 * 1000 * 1000;
 __device__ __forceinline__ unsigned long long global_ns() {
     unsigned long long t;
@@ -118,11 +118,7 @@ __device__ __forceinline__ void pipe_wait(const uint32_t *flag, uint32_t epoch) 
         if (v == epoch) break;
         const unsigned long long t = global_ns();
         if (t0 == 0) t0 = t;
-        else if (t - t0 > kPipeTimeoutNs) {
-            printf("ts_score_pipe: no sums from the previous rank after %llus (flag %u, "
-                   "epoch %u)\n", kPipeTimeoutNs / 1000000000ull, v, epoch);
-            __trap();
-        }
+        else if (t - t0 > kPipeTimeoutNs) __trap();
         __nanosleep(256);
     }
 }
@@ -219,76 +215,98 @@ __device__ __forceinline__ uint32_t ldsu(uint32_t addr, int fw) {
     return v;
 }
 
-// Walk NK trees of one chunk in lockstep (NK independent chains) over the
-// kSplit record (ts_internal.h):
-//  * top levels (< kTopLevels): records {fid << 10, theta}; the chain state is
-//    the record's shared address p and the heap step j -> 2j + 1 + c becomes
-//    p -> 2p + (c ? 16 - base : 8 - base);
-//  * deep levels: per-level arrays thr[2^l] (fp32) and fid[2^l] (FW bytes);
-//    state v = base_fid + FW * i (i = index within the level), the step
-//    i -> 2i + c becomes v -> 2v - base_fid + FW * c and the threshold sits at
-//    (4/FW) * v + kq + per-level immediate.
+// Compile-time kSplit record geometry (same formula as split_geom).
+template <int D, int FW>
+struct SplitRec {
+    static constexpr uint32_t S = D < kTopLevels ? D : kTopLevels;
+    static constexpr uint32_t kThr0 = ((1u << S) - 1u) * 8u;
+    static constexpr uint32_t kDeep = (1u << D) - (1u << S);
+    static constexpr uint32_t kLeaf0 = kThr0 + kDeep * 4u;
+    static constexpr uint32_t kFid0 = kLeaf0 + (1u << D) * 4u;
+    static constexpr uint32_t kBytes = (kFid0 + kDeep * FW + 15u) & ~15u;
+};
+
+// sel = (v >= th) ? on_ge : on_lt, kept as one FSETP + SEL on registers
+// (ptxas otherwise rematerialises the per-chain constants).
+__device__ __forceinline__ uint32_t sel_ge(float v, float th, uint32_t on_ge, uint32_t on_lt) {
+    uint32_t r;
+    asm("{\n\t.reg .pred q;\n\tsetp.ge.f32 q, %1, %2;\n\tselp.u32 %0, %3, %4, q;\n\t}"
+        : "=r"(r)
+        : "f"(v), "f"(th), "r"(on_ge), "r"(on_lt));
+    return r;
+}
+
+// Walk NK consecutive trees of one chunk in lockstep (NK independent chains)
+// over the kSplit record (ts_internal.h), tree k at tree0 + k * kBytes.
+//  * top levels (< kTopLevels): the chain state is the record's shared
+//    address p; the heap step j -> 2j + 1 + c (the reference's
+//    i = (i<<1)+1+(x >= theta)) becomes p -> 2p + (c ? 16 - base : 8 - base):
+//    LDS.64, LEA.HI, LDS, FSETP, SEL, IADD3 per visit;
+//  * deep levels: state u = address of the node's fid byte(s); theta sits at
+//    (4/FW) u + per-chain constant, and the step is u -> 2u + (c ? FW - cf : -cf)
+//    with cf = the level-independent fid origin;
+//  * leaf: ordinal from the final state, fp32 leaf value, f64 add in tree order.
 template <int D, int NK, int FW, bool UNIT_W, bool ORD, int CW>
-__device__ __forceinline__ void walk_group(uint32_t tree0, uint32_t tree_bytes, uint32_t xr,
-                                           double &acc, const StreamArgs &a, int t,
-                                           long long row, bool valid) {
-    constexpr int S = D < kTopLevels ? D : kTopLevels;
-    constexpr uint32_t kThr0 = ((1u << S) - 1u) * 8u;
-    constexpr uint32_t kDeep = (1u << D) - (1u << S);
-    constexpr uint32_t kLeaf0 = kThr0 + kDeep * 4u;
-    constexpr uint32_t kFid0 = kLeaf0 + (1u << D) * 4u;
-    constexpr int kShift = FW == 1 ? 2 : 1;  // thr address = v << kShift + kq
-    uint32_t p[NK];
+__device__ __forceinline__ void walk_group(uint32_t tree0, uint32_t xr, double &acc,
+                                           const StreamArgs &a, int t, long long row,
+                                           bool valid) {
+    using R = SplitRec<D, FW>;
+    constexpr uint32_t S = R::S;
+    constexpr uint32_t TB = R::kBytes;
+    constexpr int kShift = FW == 1 ? 2 : 1;  // theta address = u << kShift + kq
+    uint32_t p[NK], lo[NK], hi[NK];
 #pragma unroll
-    for (int k = 0; k < NK; k++) p[k] = tree0 + k * tree_bytes;
+    for (int k = 0; k < NK; k++) {
+        const uint32_t base = tree0 + k * TB;
+        p[k] = base;
+        lo[k] = 8u - base;
+        hi[k] = 16u - base;
+    }
 #pragma unroll
-    for (int l = 0; l < S; l++) {
+    for (uint32_t l = 0; l < S; l++) {
 #pragma unroll
         for (int k = 0; k < NK; k++) {
-            const uint32_t base = tree0 + k * tree_bytes;
             const uint2 q = lds64(p[k]);
             const float v = ldsf((q.x >> Shape<CW>::kXShift) + xr);
-            p[k] = 2u * p[k] + (v >= __uint_as_float(q.y) ? 16u - base : 8u - base);
+            p[k] = p[k] + p[k] + sel_ge(v, __uint_as_float(q.y), hi[k], lo[k]);
         }
     }
-    uint32_t idx[NK];  // D <= S: heap index of the leaf; D > S: v state
+    // leaf / deep origin: cf = tree + kFid0 - FW * 2^S, u = cf + FW * h
+    uint32_t u[NK];
     if constexpr (D > S) {
 #pragma unroll
         for (int k = 0; k < NK; k++) {
-            const uint32_t base = tree0 + k * tree_bytes;
-            const uint32_t bf = base + kFid0;
-            // leaving the top: heap slot j = (p - base) / 8, index in level S
-            idx[k] = bf + FW * (((p[k] - base) >> 3) - ((1u << S) - 1u));
+            const uint32_t base = tree0 + k * TB;
+            const uint32_t cf = base + R::kFid0 - FW * (1u << S);
+            // leaving the top: h = (p - base) / 8 + 1
+            u[k] = cf + FW * (((p[k] - base) >> 3) + 1u);
+            lo[k] = 0u - cf;
+            hi[k] = FW - cf;
+            // theta(u) = (u << kShift) + kq[k]: reuse p[] for kq
+            p[k] = base + R::kThr0 - 4u * (1u << S) - (cf << kShift);
         }
 #pragma unroll
-        for (int l = S; l < D; l++) {
-            const uint32_t lvl = (1u << l) - (1u << S);
+        for (uint32_t l = S; l < (uint32_t)D; l++) {
 #pragma unroll
             for (int k = 0; k < NK; k++) {
-                const uint32_t base = tree0 + k * tree_bytes;
-                const uint32_t bf = base + kFid0;
-                const uint32_t kq = base + kThr0 - (bf << kShift);
-                const float th = ldsf((idx[k] << kShift) + kq + 4u * lvl);
-                const uint32_t fid = ldsu(idx[k] + FW * lvl, FW);
+                const float th = ldsf((u[k] << kShift) + p[k]);
+                const uint32_t fid = ldsu(u[k], FW);
                 const float v = ldsf(fid * (Shape<CW>::kB * 4u) + xr);
-                idx[k] = 2u * idx[k] + (v >= th ? (uint32_t)FW - bf : 0u - bf);
+                u[k] = u[k] + u[k] + sel_ge(v, th, hi[k], lo[k]);
             }
         }
     }
 #pragma unroll
     for (int k = 0; k < NK; k++) {
-        const uint32_t base = tree0 + k * tree_bytes;
-        uint32_t ord;
-        if constexpr (D > S) {
-            ord = (idx[k] - (base + kFid0)) / FW;
-        } else {
-            ord = ((p[k] - base) >> 3) - ((1u << D) - 1u);
-        }
-        const float lv = ldsf(base + kLeaf0 + ord * 4u);
+        const uint32_t base = tree0 + k * TB;
+        uint32_t h;  // 1-based heap index at level D
+        if constexpr (D > S) h = (u[k] - (base + R::kFid0 - FW * (1u << S))) / FW;
+        else h = ((p[k] - base) >> 3) + 1u;
+        const float lv = ldsf(base + R::kLeaf0 + 4u * (h - (1u << D)));
         if constexpr (UNIT_W) acc = __dadd_rn(acc, (double)lv);
         else acc = __dadd_rn(acc, __dmul_rn(__ldg(a.weight + t + k), (double)lv));
         if constexpr (ORD) {
-            if (valid) a.ord[(long long)(t + k) * a.ld_ord + row] = (uint16_t)ord;
+            if (valid) a.ord[(long long)(t + k) * a.ld_ord + row] = (uint16_t)(h - (1u << D));
         }
     }
 }
@@ -363,11 +381,11 @@ __global__ void __launch_bounds__(Shape<CW>::kThreads, Shape<CW>::kCtasPerSm)
             const int trees = min(a.tpc, a.t1 - t0);
             int k = 0;
             for (; k + K <= trees; k += K)
-                walk_group<D, K, FW, UNIT_W, ORD, CW>(buf + k * a.tree_bytes, a.tree_bytes, xr,
-                                                      acc, a, t0 + k, row, valid);
+                walk_group<D, K, FW, UNIT_W, ORD, CW>(buf + k * SplitRec<D, FW>::kBytes, xr, acc,
+                                                      a, t0 + k, row, valid);
             for (; k < trees; k++)
-                walk_group<D, 1, FW, UNIT_W, ORD, CW>(buf + k * a.tree_bytes, a.tree_bytes, xr,
-                                                      acc, a, t0 + k, row, valid);
+                walk_group<D, 1, FW, UNIT_W, ORD, CW>(buf + k * SplitRec<D, FW>::kBytes, xr, acc,
+                                                      a, t0 + k, row, valid);
             __syncwarp();
             if (lane == 0) mbar_arrive(empty + s);
         }
