@@ -1,0 +1,20 @@
+// ts_cstream_w8.cu -- instantiations of k_cstream with 8 walker warps.
+#include "ts_cstream_kernel.cuh"
+
+namespace ts {
+namespace cstream_detail {
+
+cudaError_t launch_w8(const CStreamArgs &a, int device, cudaStream_t stream) {
+    if (a.B == 256 && a.k == 8) return launch_kgw<8, 8, 8>(a, device, stream);
+    if (a.B == 256 && a.k == 4) return launch_kgw<4, 8, 8>(a, device, stream);
+    if (a.B == 128 && a.k == 8) return launch_kgw<8, 4, 8>(a, device, stream);
+    if (a.B == 128 && a.k == 4) return launch_kgw<4, 4, 8>(a, device, stream);
+    if (a.B == 64 && a.k == 8) return launch_kgw<8, 2, 8>(a, device, stream);
+    if (a.B == 64 && a.k == 4) return launch_kgw<4, 2, 8>(a, device, stream);
+    if (a.B == 32 && a.k == 8) return launch_kgw<8, 1, 8>(a, device, stream);
+    if (a.B == 32 && a.k == 4) return launch_kgw<4, 1, 8>(a, device, stream);
+    return cudaErrorInvalidConfiguration;
+}
+
+}  // namespace cstream_detail
+}  // namespace ts

@@ -30,8 +30,10 @@ namespace ts {
 //             deeper levels as separate fp32-threshold and 1- or 2-byte fid
 //             arrays (smaller, less bank-conflicted shared-memory reads).
 //  kCStream:  kCompact for the irregular-tree streaming kernel (ts_cstream.cu):
-//             record {fid | (8 * left) << 16, theta}; leaf {F | (8 * self) << 16,
-//             value}; trees of <= 8191 nodes, grouped into chunks.
+//             record {(4 B fid) << 14 | left, theta} with B the kernel's
+//             instance tile (so 4 B fid is the feature's byte offset in the x
+//             tile, < 2^18); leaf {(4 B F) << 14 | self, value}; trees of
+//             <= 8191 nodes, grouped into chunks of <= kCStreamMaxT trees.
 enum Layout : int { kComplete = 0, kCompact = 1, kSplit = 2, kCStream = 3 };
 
 struct Segment {
@@ -40,6 +42,7 @@ struct Segment {
     int t0, t1;   // tree range [t0, t1) in evaluation order
     uint64_t byte0;  // blob offset of tree t0
     int chunk0 = 0, nchunks = 0;  // kCStream: chunk table range
+    int cs_b = 0;                 // kCStream: instance tile the records were encoded for
 };
 
 // All trees live in one byte blob, tree t at byte 16 * tree_off16[t]:
@@ -181,7 +184,7 @@ inline int split_fid_width(int F) { return F <= 256 ? 1 : 2; }
 cudaError_t launch_stream(int D, const StreamArgs &a, int device, cudaStream_t stream);
 
 // Irregular-tree streaming kernel (ts_cstream.cu).
-constexpr int kCStreamMaxT = 32;     // tree slots per chunk
+constexpr int kCStreamMaxT = 64;     // tree slots per chunk
 constexpr int kCStreamMaxNodes = 8191;
 struct CStreamArgs {
     const float *x;
@@ -193,7 +196,8 @@ struct CStreamArgs {
     const uint32_t *slot_meta;
     int chunk0, nchunks;
     int tpc;               // max trees per chunk
-    int k;                 // lockstep chains per thread (4 or 8)
+    int w;                 // walker warps (8 or 16)
+    int k;                 // lockstep chains per thread (3..8)
     uint32_t chunk_cap, stage_bytes, xs_bytes, lb_bytes;
     const double *weight;
     int unit_w, accumulate;

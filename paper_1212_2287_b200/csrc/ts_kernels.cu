@@ -273,7 +273,9 @@ cudaError_t launch_segment(const Segment &seg, const ScoreArgs &args, int device
     if (args.n <= 0) return cudaSuccess;
     if (seg.layout == kCStream) {
         CStreamArgs ca{};
-        if (!plan_cstream(args.F, device, &ca)) return cudaErrorInvalidConfiguration;
+        // the records encode x-tile offsets for the tile planned at pack time
+        if (!plan_cstream(args.F, device, &ca) || ca.B != seg.cs_b)
+            return cudaErrorInvalidConfiguration;
         ca.x = args.x;
         ca.n = args.n;
         ca.ld = args.ld;

@@ -164,9 +164,10 @@ void fill_split(const int32_t *fid, const float *val, const int32_t *lc, const i
 }
 
 // Compact BFS layout with adjacent sibling pairs and self-loop leaves.
-// child_scale 1: kCompact (child index << 16); 8: kCStream (child byte offset).
+// xstride 0: kCompact {fid | left << 16, theta}; xstride 4B: kCStream
+// {(xstride * fid) << 14 | left, theta} (ts_internal.h).
 void fill_compact(const int32_t *fid, const float *val, const int32_t *lc, const int32_t *rc,
-                  const TreeShape &s, int F, uint2 *nodes, uint32_t child_scale) {
+                  const TreeShape &s, int F, uint2 *nodes, uint32_t xstride) {
     const int32_t n = (int32_t)s.bfs.size();
     std::vector<int32_t> newid(n, -1);
     std::vector<int32_t> order;
@@ -185,8 +186,9 @@ void fill_compact(const int32_t *fid, const float *val, const int32_t *lc, const
         int32_t i = order[k];
         uint2 rec;
         memcpy(&rec.y, &val[i], 4);
-        if (fid[i] < 0) rec.x = (uint32_t)F | ((uint32_t)k * child_scale << 16);
-        else rec.x = (uint32_t)fid[i] | ((uint32_t)newid[lc[i]] * child_scale << 16);
+        const uint32_t f = fid[i] < 0 ? (uint32_t)F : (uint32_t)fid[i];
+        const uint32_t left = fid[i] < 0 ? (uint32_t)k : (uint32_t)newid[lc[i]];
+        rec.x = xstride ? (xstride * f) << 14 | left : f | left << 16;
         nodes[k] = rec;
     }
 }
@@ -310,7 +312,7 @@ extern "C" int ts_pack_ex(const ts_model_desc *d, int device, int flags, ts_mode
             fill_split(fid, val, lc, rcc, shapes[t].depth, fw, dst);
         else
             fill_compact(fid, val, lc, rcc, shapes[t], F, reinterpret_cast<uint2 *>(dst),
-                         layout[t] == kCStream ? 8u : 1u);
+                         layout[t] == kCStream ? 4u * (uint32_t)cplan.B : 0u);
     }
 
     ts_model *m = new ts_model();
@@ -339,6 +341,7 @@ extern "C" int ts_pack_ex(const ts_model_desc *d, int device, int flags, ts_mode
     for (Segment &sg : m->segments) {
         if (sg.layout != kCStream) continue;
         sg.chunk0 = (int)chunk_info.size();
+        sg.cs_b = cplan.B;
         int t = sg.t0;
         while (t < sg.t1) {
             int e = t;
