@@ -311,3 +311,16 @@ def test_invalid_models_rejected_by_packer():
     for fm in bad:
         with pytest.raises(ModelSemanticError):
             GpuModel(fm)
+
+
+@pytest.mark.parametrize("plan", ["2,8,4", "1,8,4", "1,8,8", "4,8,8", "2,16,4", "1,16,3", "8,8,4"])
+@pytest.mark.parametrize("name", ["wide_irregular", "mixed", "deep_unbalanced"])
+def test_irregular_kernel_shapes(name, plan, monkeypatch):
+    """Every k_cstream shape (G instance groups, W walker warps, K chains) the
+    planner can pick, forced with TS_CSTREAM_PLAN at pack and launch time;
+    shapes that do not fit fall back to the L1 path, which must agree too."""
+    monkeypatch.setenv("TS_CSTREAM_PLAN", plan)
+    ens, g = load_golden(name)
+    ev = _ev(ens)
+    assert np.array_equal(ev.predict_batch(g["X"]), g["scores"])
+    assert np.array_equal(ev.leaf_indices(g["X"]), g["ordinals"])
