@@ -277,9 +277,16 @@ extern "C" int ts_score_host(const ts_model *mc, const float *x, int64_t n, int6
         return cuda_fail(e, "cudaMemsetAsync");
     // The compute stream must not start before the status reset; the copy
     // stream's first wait below orders buffer reuse.
+    // Full chunks, then halving pieces over the last two chunks' worth of
+    // rows, so the part not overlapped with a copy (the last piece's kernel
+    // and D2H) is small.
     int k = 0;
-    for (int64_t r0 = 0; r0 < n; r0 += chunk, k ^= 1) {
-        const int64_t rows = std::min(chunk, n - r0);
+    int64_t rows = 0;
+    for (int64_t r0 = 0; r0 < n; r0 += rows, k ^= 1) {
+        const int64_t left = n - r0;
+        rows = left > 2 * chunk ? chunk
+                                : std::min(left, std::max<int64_t>(std::min<int64_t>(4096, chunk),
+                                                                   (left + 1) / 2));
         if ((e = cudaStreamWaitEvent(s.copy, s.consumed[k], 0)) ||
             (e = cudaMemcpyAsync(s.x[k], x + r0 * f, rows * row_bytes, cudaMemcpyHostToDevice,
                                  s.copy)) ||
