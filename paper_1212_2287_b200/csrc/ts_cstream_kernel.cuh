@@ -102,6 +102,25 @@ __device__ __forceinline__ uint32_t child_addr(uint32_t rec, uint32_t base) {
     return r;
 }
 
+// One lockstep step's loads for a chain: the record at p and the lane's
+// x value for its feature -- skipped (predicated off, no shared-memory
+// wavefront) once the previous record was a leaf: the lane is parked on its
+// self-loop leaf and q / v already hold that leaf record and the sentinel's
+// -inf, so the step below leaves p unchanged and adds a 0 ordinal bit.
+__device__ __forceinline__ void walk_loads(uint2 &q, float &v, uint32_t p, uint32_t xr,
+                                           uint32_t leafmark) {
+    TS_DBG(p, 8);
+    asm volatile(
+        "{\n\t.reg .pred live;\n\t.reg .u32 a;\n\t"
+        "setp.lt.u32 live, %0, %4;\n\t"
+        "@live ld.shared.v2.u32 {%0, %1}, [%3];\n\t"
+        "shr.u32 a, %0, 14;\n\t"
+        "add.u32 a, a, %5;\n\t"
+        "@live ld.shared.f32 %2, [a];\n\t}"
+        : "+r"(q.x), "+r"(q.y), "+f"(v)
+        : "r"(p), "r"(leafmark), "r"(xr));
+}
+
 template <int kK, int G, int W, bool UNIT_W, bool ORD>
 __global__ void __launch_bounds__(threads_c(W), 1) k_cstream(CStreamArgs a) {
     // G (instance groups of 32, B = 32 * G) is a template parameter so the
@@ -199,6 +218,8 @@ __global__ void __launch_bounds__(threads_c(W), 1) k_cstream(CStreamArgs a) {
     const int inst = grp * 32 + lane;
     const uint32_t xr = su32(xs) + 4u * inst;
     const uint32_t lbase0 = su32(lb0);
+    // records at or above leafmark are leaves (x offset of the sentinel row F)
+    const uint32_t leafmark = ((uint32_t)a.F * (uint32_t)(4 * B)) << 14;
     uint32_t it = 0;
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const long long row0 = tile * B;
@@ -224,6 +245,8 @@ __global__ void __launch_bounds__(threads_c(W), 1) k_cstream(CStreamArgs a) {
             const int rot = (sub + c) % S;
             for (int s0 = rot * kK; s0 < (int)nt; s0 += S * kK) {
                 uint32_t p[kK], tb[kK], tb8[kK], ob[kK], rel[kK];
+                uint2 q[kK];
+                float v[kK];
                 int dk[kK];
                 int dmax = 0;
 #pragma unroll
@@ -239,15 +262,16 @@ __global__ void __launch_bounds__(threads_c(W), 1) k_cstream(CStreamArgs a) {
                     dk[k] = (m >> 16) & 31;
                     dmax = max(dmax, dk[k]);
                     ob[k] = 0;
+                    q[k] = make_uint2(0u, 0u);  // "not on a leaf"
+                    v[k] = 0.f;
                 }
 #pragma unroll 1
                 for (int l = 0; l < dmax; l++) {
 #pragma unroll
                     for (int k = 0; k < kK; k++) {
-                        const uint2 q = lds64(p[k]);
-                        const float v = ldsf((q.x >> 14) + xr);
-                        const bool c = v >= __uint_as_float(q.y);
-                        p[k] = child_addr(q.x, c ? tb8[k] : tb[k]);
+                        walk_loads(q[k], v[k], p[k], xr, leafmark);
+                        const bool c = v[k] >= __uint_as_float(q[k].y);
+                        p[k] = child_addr(q[k].x, c ? tb8[k] : tb[k]);
                         if constexpr (ORD) ob[k] = 2u * ob[k] + (c ? 1u : 0u);
                     }
                 }
