@@ -43,9 +43,8 @@ __host__ __device__ constexpr int threads_c(int W) { return 32 * W + 64; }
 
 // Stage B rows x F features into xs[f * B + r] (+ sentinel row F = -inf),
 // all walker threads cooperating.
-template <int NT>
+template <int NT, int B>
 __device__ __forceinline__ void stage_rows_c(const CStreamArgs &a, float *xs, long long row0) {
-    const int B = a.B;
     const int F = a.F;
     const int tid = threadIdx.x;
     bool bad = false;
@@ -224,7 +223,7 @@ __global__ void __launch_bounds__(threads_c(W), 1) k_cstream(CStreamArgs a) {
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const long long row0 = tile * B;
         consumer_sync<kConsumers>();  // all walks of the previous tile are done
-        stage_rows_c<kConsumers>(a, xs, row0);
+        stage_rows_c<kConsumers, B>(a, xs, row0);
         consumer_sync<kConsumers>();
         const long long walk_row = row0 + inst;
         const bool walk_valid = walk_row < a.n;

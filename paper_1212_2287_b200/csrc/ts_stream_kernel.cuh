@@ -337,17 +337,23 @@ __global__ void __launch_bounds__(Shape<CW>::kThreads, Shape<CW>::kCtasPerSm)
 
     if (warp == kConsumerWarps) {  // ---- producer warp: TMA bulk copies
         if (lane == 0) {
-            uint32_t it = 0;
+            // ring position tracked incrementally (no runtime division)
+            int s = 0;
+            uint32_t ph = 0, used = 0;  // phase of stage s's next reuse; first lap done?
             for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-                for (int c = 0; c < nchunks; c++, it++) {
-                    const int s = it % kStages;
-                    if (it >= kStages) mbar_wait(empty + s, ((it / kStages) - 1) & 1);
+                for (int c = 0; c < nchunks; c++) {
+                    if (used) mbar_wait(empty + s, ph);
                     const int trees = min(a.tpc, a.t1 - a.t0 - c * a.tpc);
                     const uint32_t bytes = (uint32_t)trees * a.tree_bytes;
                     mbar_expect_tx(full + s, bytes);
                     bulk_g2s(ring + s * a.chunk_cap,
                              a.blob + a.seg_byte0 + (size_t)c * a.tpc * a.tree_bytes, bytes,
                              full + s);
+                    if (++s == kStages) {
+                        s = 0;
+                        ph ^= used;
+                        used = 1;
+                    }
                 }
             }
         }
@@ -357,7 +363,8 @@ __global__ void __launch_bounds__(Shape<CW>::kThreads, Shape<CW>::kCtasPerSm)
     // ---- consumer warps
     const int r = threadIdx.x;
     const uint32_t xr = su32(xs) + 4u * r;
-    uint32_t it = 0;
+    int s = 0;
+    uint32_t ph = 0;  // parity of stage s's current fill
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const long long row = tile * kB + r;
         const bool valid = row < a.n;
@@ -373,9 +380,8 @@ __global__ void __launch_bounds__(Shape<CW>::kThreads, Shape<CW>::kCtasPerSm)
             __syncwarp();
             acc = valid ? __ldcv(a.pipe.sums_in + row) : 0.0;
         }
-        for (int c = 0; c < nchunks; c++, it++) {
-            const int s = it % kStages;
-            mbar_wait(full + s, (it / kStages) & 1);
+        for (int c = 0; c < nchunks; c++) {
+            mbar_wait(full + s, ph);
             const uint32_t buf = su32(ring + s * a.chunk_cap);
             const int t0 = a.t0 + c * a.tpc;
             const int trees = min(a.tpc, a.t1 - t0);
@@ -388,6 +394,10 @@ __global__ void __launch_bounds__(Shape<CW>::kThreads, Shape<CW>::kCtasPerSm)
                                                       a, t0 + k, row, valid);
             __syncwarp();
             if (lane == 0) mbar_arrive(empty + s);
+            if (++s == kStages) {
+                s = 0;
+                ph ^= 1u;
+            }
         }
         if (a.pipe.sums_out) {
             // publish to the next rank (peer memory over NVLink), then flag
