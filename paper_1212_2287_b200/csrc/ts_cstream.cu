@@ -19,10 +19,15 @@ cudaError_t launch_w16(const CStreamArgs &a, int device, cudaStream_t stream);
 }  // namespace cstream_detail
 
 // Kernel shape: the most lockstep chains (W walker warps x K trees) whose
-// instance tile, double-buffered leaf buffer and two ring stages of
-// tpc = (W / G) * K trees (~1.2 KB per 64-leaf tree) fit the opt-in shared
-// memory; ties go to the larger tile (fewer tree-stream passes), then to more
-// warps.  TS_CSTREAM_PLAN=G,W,K forces one shape (A/B experiments).
+// instance tile, double-buffered leaf buffer and >= 2 ring stages of tpc
+// trees (~1.2 KB per 64-leaf tree) fit the opt-in shared memory, with tpc =
+// S*K trees per chunk (every walker warp on every chunk, S = W/G).  Ties go
+// to more stages (up to 3), then the larger tile (fewer tree-stream passes),
+// then more warps.  Two teams on alternate chunks of S*K/2 trees (smaller
+// stages, more of them in flight) are only a fallback: on config 3 the
+// 16x4 two-team shape ran 58.8 ms against 57.8 ms for 16x3 with one team
+// (per-chunk overhead is paid per half as much work).
+// TS_CSTREAM_PLAN=G,W,K[,teams] forces a shape (A/B experiments).
 bool plan_cstream(int F, int device, CStreamArgs *a) {
     using namespace cstream_detail;
     const int optin = dev_attrs(device).smem_optin;
@@ -31,41 +36,54 @@ bool plan_cstream(int F, int device, CStreamArgs *a) {
     static const Cand cands[] = {{8, 8, 8}, {8, 8, 4}, {4, 8, 8}, {4, 8, 4}, {2, 8, 8},
                                  {2, 8, 4}, {1, 8, 8}, {1, 8, 4}, {2, 16, 4}, {2, 16, 3},
                                  {1, 16, 4}, {1, 16, 3}};
-    int fg = 0, fw = 0, fk = 0;
-    if (const char *e = getenv("TS_CSTREAM_PLAN")) sscanf(e, "%d,%d,%d", &fg, &fw, &fk);
+    int fg = 0, fw = 0, fk = 0, ft = 0;
+    if (const char *e = getenv("TS_CSTREAM_PLAN")) sscanf(e, "%d,%d,%d,%d", &fg, &fw, &fk, &ft);
     bool found = false;
     CStreamArgs best{};
-    int best_chains = 0;
+    long best_key = -1;
     for (const Cand &c : cands) {
         if (fg && (c.G != fg || c.W != fw || c.K != fk)) continue;
-        const int B = 32 * c.G;
-        const int S = c.W / c.G;
-        const int tpc = std::min(S * c.K, kCStreamMaxT);
-        const size_t xs = ((size_t)(F + 1) * B * 4 + 127) & ~(size_t)127;
-        const size_t lb = 2 * (size_t)tpc * B * 4;  // double-buffered
-        const size_t bars = 8 * 8;
-        if (xs + lb + bars >= (size_t)optin) continue;
-        const size_t stage = ((((size_t)optin - xs - lb - bars) / kStagesC) & ~(size_t)127);
-        if (stage < kHeadBytes + (size_t)tpc * 1200) continue;
-        const int chains = c.W * c.K;
-        if (found && (chains < best_chains || (chains == best_chains && B <= best.B))) continue;
-        found = true;
-        best_chains = chains;
-        best = CStreamArgs{};
-        best.B = B;
-        best.w = c.W;
-        best.k = c.K;
-        best.tpc = tpc;
-        best.xs_bytes = (uint32_t)xs;
-        best.lb_bytes = (uint32_t)lb;
-        best.stage_bytes = (uint32_t)std::min<size_t>(stage, (size_t)tpc * 2048 + kHeadBytes);
-        best.chunk_cap = best.stage_bytes - kHeadBytes;  // tree bytes per stage
+        for (int teams = 1; teams <= 2; teams++) {
+            if (ft && teams != ft) continue;
+            const int B = 32 * c.G;
+            const int S = c.W / c.G;
+            if (S % teams) continue;
+            const int tpc = std::min(S * c.K / teams, kCStreamMaxT);
+            const size_t xs = ((size_t)(F + 1) * B * 4 + 127) & ~(size_t)127;
+            const size_t lb = 2 * (size_t)tpc * B * 4;  // double-buffered
+            const size_t bars = (2 * kMaxStagesC + 4) * 8;
+            if (xs + lb + bars >= (size_t)optin) continue;
+            const size_t need = kHeadBytes + (size_t)tpc * 1200;   // one chunk of trees
+            const size_t room = (size_t)optin - xs - lb - bars;
+            const int stages = (int)std::min<size_t>(kMaxStagesC, room / ((need + 127) & ~(size_t)127));
+            if (stages < 2) continue;
+            const size_t stage = std::min<size_t>((room / stages) & ~(size_t)127,
+                                                  (size_t)tpc * 2048 + kHeadBytes);
+            const long key = (2 - teams) * 1000000000L + (long)c.W * c.K * 1000000 +
+                             std::min(stages, 3) * 100000 + B * 100 + c.W * 2;
+            if (found && key <= best_key) continue;
+            found = true;
+            best_key = key;
+            best = CStreamArgs{};
+            best.B = B;
+            best.w = c.W;
+            best.k = c.K;
+            best.tpc = tpc;
+            best.stages = stages;
+            best.teams = teams;
+            best.xs_bytes = (uint32_t)xs;
+            best.lb_bytes = (uint32_t)lb;
+            best.stage_bytes = (uint32_t)stage;
+            best.chunk_cap = best.stage_bytes - kHeadBytes;  // tree bytes per stage
+        }
     }
     if (!found) return false;
     a->B = best.B;
     a->w = best.w;
     a->k = best.k;
     a->tpc = best.tpc;
+    a->stages = best.stages;
+    a->teams = best.teams;
     a->xs_bytes = best.xs_bytes;
     a->lb_bytes = best.lb_bytes;
     a->stage_bytes = best.stage_bytes;

@@ -36,7 +36,7 @@ namespace cstream_detail {
 
 using namespace stream_detail;
 
-constexpr int kStagesC = 2;
+constexpr int kMaxStagesC = 4;
 constexpr uint32_t kMetaBytes = kCStreamMaxT * 4;  // slot table at the head of a stage
 constexpr uint32_t kHeadBytes = kMetaBytes + 16;   // + the chunk's chunk_info entry
 __host__ __device__ constexpr int threads_c(int W) { return 32 * W + 64; }
@@ -130,14 +130,15 @@ __global__ void __launch_bounds__(threads_c(W), 1) k_cstream(CStreamArgs a) {
     float *xs = reinterpret_cast<float *>(smem);
     float *lb0 = reinterpret_cast<float *>(smem + a.xs_bytes);  // two leaf buffers
     unsigned char *ring = smem + a.xs_bytes + a.lb_bytes;
-    uint64_t *full = reinterpret_cast<uint64_t *>(ring + kStagesC * a.stage_bytes);
-    uint64_t *empty = full + kStagesC;  // ring stage consumed (W walker warps)
-    uint64_t *lbf = empty + kStagesC;   // leaf buffer written (W walker warps)
+    const int nst = a.stages;  // ring stages (2-4)
+    uint64_t *full = reinterpret_cast<uint64_t *>(ring + nst * a.stage_bytes);
+    uint64_t *empty = full + kMaxStagesC;  // ring stage consumed (W walker warps)
+    uint64_t *lbf = empty + kMaxStagesC;   // leaf buffer written (W walker warps)
     uint64_t *lbe = lbf + 2;            // leaf buffer folded (accumulator warp)
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kStagesC; s++) {
+        for (int s = 0; s < nst; s++) {
             mbar_init(full + s, 1);
             mbar_init(empty + s, W);
         }
@@ -154,11 +155,11 @@ __global__ void __launch_bounds__(threads_c(W), 1) k_cstream(CStreamArgs a) {
 
     if (warp == W + 1) {  // ---- producer: TMA bulk copies per chunk
         if (lane == 0) {
-            uint32_t it = 0;
+            int s = 0;
+            uint32_t ph = 0, used = 0;  // phase of stage s's next reuse; first lap done?
             for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-                for (int c = 0; c < a.nchunks; c++, it++) {
-                    const int s = it % kStagesC;
-                    if (it >= kStagesC) mbar_wait(empty + s, ((it / kStagesC) - 1) & 1);
+                for (int c = 0; c < a.nchunks; c++) {
+                    if (used) mbar_wait(empty + s, ph);
                     const uint4 ci = __ldg(a.chunk_info + a.chunk0 + c);
                     unsigned char *stage = ring + s * a.stage_bytes;
                     mbar_expect_tx(full + s, ci.y + kMetaBytes + 16);
@@ -166,6 +167,11 @@ __global__ void __launch_bounds__(threads_c(W), 1) k_cstream(CStreamArgs a) {
                              kMetaBytes, full + s);
                     bulk_g2s(stage + kMetaBytes, a.chunk_info + a.chunk0 + c, 16, full + s);
                     bulk_g2s(stage + kHeadBytes, a.blob + 16ull * ci.x, ci.y, full + s);
+                    if (++s == nst) {
+                        s = 0;
+                        ph ^= used;
+                        used = 1;
+                    }
                 }
             }
         }
@@ -219,6 +225,13 @@ __global__ void __launch_bounds__(threads_c(W), 1) k_cstream(CStreamArgs a) {
     const uint32_t lbase0 = su32(lb0);
     // records at or above leafmark are leaves (x offset of the sentinel row F)
     const uint32_t leafmark = ((uint32_t)a.F * (uint32_t)(4 * B)) << 14;
+    // teams: a.teams (1 or 2) sets of SR = S / teams warps per instance group
+    const int team_shift = a.teams == 2 ? 1 : 0;
+    const uint32_t team_mask = (uint32_t)a.teams - 1u;
+    const int SR = S >> team_shift;
+    const int team = sub / SR, sidx = sub % SR;
+    int s = 0;
+    uint32_t ph = 0;  // parity of stage s's current fill
     uint32_t it = 0;
     for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const long long row0 = tile * B;
@@ -228,10 +241,9 @@ __global__ void __launch_bounds__(threads_c(W), 1) k_cstream(CStreamArgs a) {
         const long long walk_row = row0 + inst;
         const bool walk_valid = walk_row < a.n;
         for (int c = 0; c < a.nchunks; c++, it++) {
-            const int s = it % kStagesC;
             const int b = it & 1;
             const uint32_t lbase = lbase0 + b * lb_half;
-            mbar_wait(full + s, (it / kStagesC) & 1);
+            mbar_wait(full + s, ph);
             const uint32_t meta = su32(ring + s * a.stage_bytes);
             uint32_t nt, tree0;
             asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(nt), "=r"(tree0)
@@ -240,9 +252,12 @@ __global__ void __launch_bounds__(threads_c(W), 1) k_cstream(CStreamArgs a) {
             bool waited = it < 2;  // this leaf buffer's previous fold must be done
             // K-groups of K consecutive (depth-sorted) slots, so a group's
             // trees have nearly equal depth; the group a warp takes rotates
-            // with the chunk so no warp always draws the deepest trees.
-            const int rot = (sub + c) % S;
-            for (int s0 = rot * kK; s0 < (int)nt; s0 += S * kK) {
+            // with the chunk so no warp always draws the deepest trees.  With
+            // two teams (chunks of S*K/2 trees, more ring stages in flight)
+            // the teams take alternate chunks.
+            const bool mine = (int)(it & team_mask) == team;
+            const int rot = (int)((sidx + (it >> team_shift)) & (SR - 1));
+            for (int s0 = mine ? rot * kK : (int)nt; s0 < (int)nt; s0 += SR * kK) {
                 uint32_t p[kK], tb[kK], tb8[kK], ob[kK], rel[kK];
                 uint2 q[kK];
                 float v[kK];
@@ -299,12 +314,17 @@ __global__ void __launch_bounds__(threads_c(W), 1) k_cstream(CStreamArgs a) {
                 mbar_arrive(empty + s);  // ring stage read
                 mbar_arrive(lbf + b);    // leaves published (release orders the stores)
             }
+            if (++s == nst) {
+                s = 0;
+                ph ^= 1u;
+            }
         }
     }
 }
 
 inline size_t cstream_smem(const CStreamArgs &a) {
-    return (size_t)a.xs_bytes + a.lb_bytes + (size_t)kStagesC * a.stage_bytes + 8 * 8;
+    return (size_t)a.xs_bytes + a.lb_bytes + (size_t)a.stages * a.stage_bytes +
+           (2 * kMaxStagesC + 4) * 8;
 }
 
 template <int K, int G, int W>

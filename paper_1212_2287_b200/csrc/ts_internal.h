@@ -197,6 +197,8 @@ struct CStreamArgs {
     int chunk0, nchunks;
     int tpc;               // max trees per chunk
     int w;                 // walker warps (8 or 16)
+    int stages;            // ring stages (2-4)
+    int teams;             // 1: every walker warp on every chunk; 2: alternate chunks
     int k;                 // lockstep chains per thread (3..8)
     uint32_t chunk_cap, stage_bytes, xs_bytes, lb_bytes;
     const double *weight;
