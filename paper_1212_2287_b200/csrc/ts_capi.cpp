@@ -48,6 +48,29 @@ const DevAttrs &dev_attrs(int device) {
     return cache[device];
 }
 
+// The library's own stream-ordered pool for per-call scratch (tree-split
+// mode), keeping up to 512 MB between calls so a cudaMallocFromPoolAsync is a
+// sub-allocation, not a fresh mapping, and leaving the process's default pool
+// settings alone.
+cudaMemPool_t scratch_pool(int device) {
+    static cudaMemPool_t pools[64];
+    static std::once_flag once[64];
+    if (device < 0 || device >= 64) device = 0;
+    std::call_once(once[device], [device] {
+        cudaMemPoolProps props = {};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = device;
+        if (cudaMemPoolCreate(&pools[device], &props) != cudaSuccess) {
+            pools[device] = nullptr;
+            return;
+        }
+        uint64_t keep = 512ull << 20;
+        cudaMemPoolSetAttribute(pools[device], cudaMemPoolAttrReleaseThreshold, &keep);
+    });
+    return pools[device];
+}
+
 cudaError_t ensure_smem(const void *kernel, size_t bytes) {
     static std::mutex mu;
     static std::unordered_map<const void *, size_t> granted[64];  // per device

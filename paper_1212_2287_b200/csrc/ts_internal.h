@@ -177,6 +177,13 @@ struct StreamArgs {
     long long ld_ord;
     int32_t *status;
     PipeArgs pipe;
+    // > 1: small-batch tree split -- CTA b walks tile b % tiles over chunk
+    // range b / tiles of `splits`, writing each leaf value to leaf_out
+    // ([row / 32][tree - t0][row % 32], leaf_T trees) instead of summing (out
+    // unused); k_fold (ts_stream.cu) then sums them in tree order.
+    int splits;
+    float *leaf_out;
+    long long leaf_T;
 };
 // n: rows of the launch (-1 at pack time: shape-independent checks only).
 bool plan_stream(int F, int D, int device, StreamArgs *a, long long n = -1);
@@ -224,6 +231,7 @@ struct DevAttrs {
     int smem_optin = 0;
 };
 const DevAttrs &dev_attrs(int device);
+cudaMemPool_t scratch_pool(int device);  // nullptr if the device has no pool support
 
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) only when a kernel needs
 // more than it was last granted.

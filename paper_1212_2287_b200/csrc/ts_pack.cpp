@@ -12,6 +12,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 #include <string>
 #include <vector>
@@ -270,7 +271,8 @@ extern "C" int ts_pack_ex(const ts_model_desc *d, int device, int flags, ts_mode
         if (rc) return rc;
         const TreeShape &s = shapes[t];
         const int64_t nn = (int64_t)s.bfs.size();
-        if (s.complete || !compact_ok_f || nn > 65535) {
+        static const bool force_cs = getenv("TS_FORCE_CSTREAM") != nullptr;  // A/B only
+        if ((s.complete && !force_cs) || !compact_ok_f || nn > 65535) {
             layout[t] = split_ok[s.depth] ? kSplit : kComplete;
             n_complete++;
         } else {

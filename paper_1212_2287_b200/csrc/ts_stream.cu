@@ -105,9 +105,109 @@ bool plan_stream(int F, int D, int device, StreamArgs *a, long long n) {
     return plan_stream_cw(F, D, optin, 8, a);
 }
 
-cudaError_t launch_stream(int D, const StreamArgs &a, int device, cudaStream_t stream) {
-    if (a.n <= 0) return cudaSuccess;
-    return stream_detail::kStreamTable[D](a, device, stream);
+namespace {
+// Tree-order f64 fold of a tree-split launch (ref evaluators.py:529-535):
+// one CTA per 32 rows; all 8 warps stream the rows' leaf values
+// ([row/32][tree][row%32], 128 B per tree) into a double-buffered shared
+// tile with cp.async while warp 0 folds the previous tile, one lane per row,
+// acc = acc + w * leaf in tree order (__dmul_rn / __dadd_rn).
+constexpr int kFoldTrees = 128;  // trees per shared tile (16 KB)
+__device__ __forceinline__ void fold_load(float *dst, const float *src, int trees) {
+    // trees * 32 floats = trees * 8 16-byte pieces over 256 threads
+    const uint32_t d0 = (uint32_t)__cvta_generic_to_shared(dst);
+    for (int i = threadIdx.x; i < trees * 8; i += blockDim.x)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d0 + 16u * i),
+                     "l"(src + 4 * i)
+                     : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(256) k_fold(const float *leaf, long long T, int t0,
+                                              const double *weight, int unit_w, int accumulate,
+                                              double *out, long long n) {
+    __shared__ __align__(16) float tile[2][kFoldTrees * 32];
+    const long long blk = blockIdx.x;
+    const long long row = blk * 32 + (threadIdx.x & 31);
+    const float *src = leaf + blk * T * 32;
+    double acc = 0.0;
+    if (threadIdx.x < 32 && accumulate && row < n) acc = out[row];
+    const int ntile = (int)((T + kFoldTrees - 1) / kFoldTrees);
+    fold_load(tile[0], src, (int)min(T, (long long)kFoldTrees));
+    for (int i = 0; i < ntile; i++) {
+        const int tb = i * kFoldTrees;
+        const int nt = (int)min(T - tb, (long long)kFoldTrees);
+        if (i + 1 < ntile) {
+            fold_load(tile[(i + 1) & 1], src + (long long)(tb + kFoldTrees) * 32,
+                      (int)min(T - tb - kFoldTrees, (long long)kFoldTrees));
+            asm volatile("cp.async.wait_group 1;" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+        }
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            const float *lv = tile[i & 1] + threadIdx.x;
+            if (unit_w) {
+                for (int t = 0; t < nt; t++) acc = __dadd_rn(acc, (double)lv[t * 32]);
+            } else {
+                for (int t = 0; t < nt; t++)
+                    acc = __dadd_rn(acc, __dmul_rn(__ldg(weight + t0 + tb + t), (double)lv[t * 32]));
+            }
+        }
+        __syncthreads();  // tile (i & 1) is refilled next iteration
+    }
+    if (threadIdx.x < 32 && row < n) out[row] = acc;
+}
+}  // namespace
+
+// Small batches leave most SMs idle (one CTA walks ALL trees of its tile), so
+// when the tiles fill less than half of the resident CTA slots the segment's
+// chunks are split over `splits` CTAs per tile: phase 1 walks and stores each
+// leaf value (stream-ordered scratch from the device's memory pool), phase 2
+// (k_fold) sums them in tree order -- bit-identical to the one-pass kernel.
+// TS_SPLIT=0 disables, TS_SPLIT=J forces J splits (A/B experiments).
+cudaError_t launch_stream(int D, const StreamArgs &a0, int device, cudaStream_t stream) {
+    if (a0.n <= 0) return cudaSuccess;
+    StreamArgs a = a0;
+    a.splits = 1;
+    a.leaf_out = nullptr;
+    const long long B = 32ll * a.cw;
+    const long long tiles = (a.n + B - 1) / B;
+    const int resident = dev_attrs(device).sms * (a.cw == 4 ? 2 : 1);
+    const int T = a.t1 - a.t0;
+    const int nchunks = (T + a.tpc - 1) / a.tpc;
+    // worth it only when a tile's walk is long (>= 2048 node visits per row)
+    const bool long_walk = (long long)T * D >= 2048;
+    int splits = (long_walk && tiles * 2 <= resident)
+                     ? (int)std::min<long long>(nchunks, resident / tiles) : 1;
+    if (const char *e = getenv("TS_SPLIT")) {
+        const int f = atoi(e);
+        splits = f <= 0 ? 1 : std::min(f, nchunks);
+    }
+    const long long blocks = (a.n + 31) / 32;
+    const size_t scratch_bytes = (size_t)blocks * 32 * (size_t)T * sizeof(float);
+    if (splits < 2 || a.pipe.flags_in || a.pipe.sums_out || scratch_bytes > (256u << 20))
+        return stream_detail::kStreamTable[D](a, device, stream);
+
+    cudaMemPool_t pool = scratch_pool(device);
+    if (!pool) return stream_detail::kStreamTable[D](a, device, stream);
+    float *scratch = nullptr;
+    cudaError_t e = cudaMallocFromPoolAsync((void **)&scratch, scratch_bytes, pool, stream);
+    if (e != cudaSuccess) return e;
+    StreamArgs w = a;
+    w.splits = splits;
+    w.leaf_out = scratch;
+    w.leaf_T = T;
+    w.out = nullptr;
+    w.accumulate = 0;
+    e = stream_detail::kStreamTable[D](w, device, stream);
+    if (e == cudaSuccess) {
+        k_fold<<<(unsigned)blocks, 256, 0, stream>>>(scratch, T, a.t0, a.weight, a.unit_w,
+                                                      a.accumulate, a.out, a.n);
+        count_launch();
+        e = cudaGetLastError();
+    }
+    const cudaError_t f = cudaFreeAsync(scratch, stream);
+    return e != cudaSuccess ? e : f;
 }
 
 }  // namespace ts

@@ -306,7 +306,9 @@ __device__ __forceinline__ void walk_group(uint32_t tree0, uint32_t xr, double &
         if constexpr (UNIT_W) acc = __dadd_rn(acc, (double)lv);
         else acc = __dadd_rn(acc, __dmul_rn(__ldg(a.weight + t + k), (double)lv));
         if constexpr (ORD) {
-            if (valid) a.ord[(long long)(t + k) * a.ld_ord + row] = (uint16_t)(h - (1u << D));
+            if (a.ord && valid) a.ord[(long long)(t + k) * a.ld_ord + row] = (uint16_t)(h - (1u << D));
+            if (a.leaf_out)  // tree-split mode: [row / 32][tree][row % 32] for k_fold
+                a.leaf_out[((row >> 5) * a.leaf_T + (t + k - a.t0)) * 32 + (row & 31)] = lv;
         }
     }
 }
@@ -334,14 +336,26 @@ __global__ void __launch_bounds__(Shape<CW>::kThreads, Shape<CW>::kCtasPerSm)
     __syncthreads();
     const long long ntiles = (a.n + kB - 1) / kB;
     const int nchunks = (a.t1 - a.t0 + a.tpc - 1) / a.tpc;
+    // Tiles this CTA owns and the chunk range it walks: all chunks of tiles
+    // blockIdx.x, +gridDim.x, ... normally; one tile and 1/splits of the
+    // chunks in small-batch tree-split mode.
+    long long tile0 = blockIdx.x, tstep = gridDim.x;
+    int cb = 0, ce = nchunks;
+    if (a.splits > 1) {
+        tile0 = blockIdx.x % ntiles;
+        tstep = ntiles;
+        const long long j = blockIdx.x / ntiles;
+        cb = (int)(j * nchunks / a.splits);
+        ce = (int)((j + 1) * nchunks / a.splits);
+    }
 
     if (warp == kConsumerWarps) {  // ---- producer warp: TMA bulk copies
         if (lane == 0) {
             // ring position tracked incrementally (no runtime division)
             int s = 0;
             uint32_t ph = 0, used = 0;  // phase of stage s's next reuse; first lap done?
-            for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-                for (int c = 0; c < nchunks; c++) {
+            for (long long tile = tile0; tile < ntiles; tile += tstep) {
+                for (int c = cb; c < ce; c++) {
                     if (used) mbar_wait(empty + s, ph);
                     const int trees = min(a.tpc, a.t1 - a.t0 - c * a.tpc);
                     const uint32_t bytes = (uint32_t)trees * a.tree_bytes;
@@ -365,7 +379,7 @@ __global__ void __launch_bounds__(Shape<CW>::kThreads, Shape<CW>::kCtasPerSm)
     const uint32_t xr = su32(xs) + 4u * r;
     int s = 0;
     uint32_t ph = 0;  // parity of stage s's current fill
-    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    for (long long tile = tile0; tile < ntiles; tile += tstep) {
         const long long row = tile * kB + r;
         const bool valid = row < a.n;
         consumer_sync<kB>();  // previous tile's walks are done with xs
@@ -380,7 +394,7 @@ __global__ void __launch_bounds__(Shape<CW>::kThreads, Shape<CW>::kCtasPerSm)
             __syncwarp();
             acc = valid ? __ldcv(a.pipe.sums_in + row) : 0.0;
         }
-        for (int c = 0; c < nchunks; c++) {
+        for (int c = cb; c < ce; c++) {
             mbar_wait(full + s, ph);
             const uint32_t buf = su32(ring + s * a.chunk_cap);
             const int t0 = a.t0 + c * a.tpc;
@@ -405,7 +419,7 @@ __global__ void __launch_bounds__(Shape<CW>::kThreads, Shape<CW>::kCtasPerSm)
             __threadfence_system();
             __syncwarp();
             if (lane == 0 && blk < a.pipe.nblocks) pipe_signal(a.pipe.flags_out + blk, a.pipe.epoch);
-        } else if (valid) {
+        } else if (valid && a.out) {
             a.out[row] = acc;
         }
     }
@@ -414,7 +428,7 @@ __global__ void __launch_bounds__(Shape<CW>::kThreads, Shape<CW>::kCtasPerSm)
 template <int D, int FW, int CW>
 auto pick_kernel(const StreamArgs &a) {
     constexpr int K = chains_for_depth(D);
-    if (a.ord)
+    if (a.ord || a.leaf_out)
         return a.unit_w ? k_stream<D, K, FW, true, true, CW> : k_stream<D, K, FW, false, true, CW>;
     return a.unit_w ? k_stream<D, K, FW, true, false, CW> : k_stream<D, K, FW, false, false, CW>;
 }
@@ -431,7 +445,9 @@ cudaError_t launch_dc(const StreamArgs &a, int device, cudaStream_t stream) {
     e = ensure_smem((const void *)kern, smem);
     if (e != cudaSuccess) return e;
     const long long tiles = (a.n + kB - 1) / kB;
-    const int grid = (int)(tiles < (long long)sms * kCtasPerSm ? tiles : (long long)sms * kCtasPerSm);
+    const int grid = a.splits > 1 ? (int)(tiles * a.splits)
+                                  : (int)(tiles < (long long)sms * kCtasPerSm
+                                              ? tiles : (long long)sms * kCtasPerSm);
     kern<<<grid, kThreads, smem, stream>>>(a);
     count_launch();
     return cudaGetLastError();

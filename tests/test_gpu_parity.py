@@ -325,3 +325,25 @@ def test_irregular_kernel_shapes(name, plan, monkeypatch):
     ev = _ev(ens)
     assert np.array_equal(ev.predict_batch(g["X"]), g["scores"])
     assert np.array_equal(ev.leaf_indices(g["X"]), g["ordinals"])
+
+
+@pytest.mark.parametrize("split", [None, "0", "2", "7"])
+@pytest.mark.parametrize("n", [1, 100, 1000, 5000])
+def test_small_batch_tree_split(n, split, monkeypatch):
+    """Small batches split each tile's trees over several CTAs and fold the
+    leaves in tree order afterwards (TS_SPLIT forces / disables it); scores
+    and ordinals must not depend on it."""
+    from paper_1212_2287_b200.synth import complete_flat
+    if split is not None:
+        monkeypatch.setenv("TS_SPLIT", split)
+    rng = np.random.default_rng(n)
+    T, d, F = 300, 6, 40
+    n_int = (1 << d) - 1
+    flat = complete_flat(F, d, rng.integers(0, F, (T, n_int)), rng.random((T, n_int)),
+                         rng.standard_normal((T, 1 << d)), weights=rng.uniform(0.5, 1.5, T))
+    x = rng.random((n, F), dtype=np.float32)
+    ev = _ev(flat)
+    ref = oracle.COracle(flat.arrays())
+    s, o = ref.score(x, threads=4, with_ordinals=True)
+    assert np.array_equal(ev.predict_batch(x), s)
+    assert np.array_equal(ev.leaf_indices(x), o.astype(np.int64))
