@@ -1,13 +1,15 @@
 """Multi-GPU scale-out (BASELINE config 4), one process per GPU:
 
     torchrun --nproc-per-node N --master-addr 127.0.0.1 tools/bench_multi.py \
-        --mode instance|tree-reduce|tree-pipeline [--rows R] [--reps K]
+        --mode instance|tree-reduce|tree-pipeline|tree-p2p [--rows R] [--reps K]
 
 instance: config 4a (64M x 136, T=1000 d=8), each rank generates and scores
 its contiguous row shard in place on its GPU (no collective on the data path).
 tree-*: config 4b (8M x 136, T=20,000 d=10), each rank holds a balanced tree
 shard and scores all rows; partials combined by an NCCL f64 sum-reduce
-("tree-reduce") or by the bit-exact rank-to-rank pipeline ("tree-pipeline").
+("tree-reduce"), by the bit-exact rank-to-rank pipeline over NCCL
+send/recv ("tree-pipeline"), or by the same bit-exact pipeline fused into
+the scoring kernel over NVLink peer memory ("tree-p2p", ts_score_pipe).
 Timing: barrier + synchronize around K passes, CUDA events, max over ranks.
 """
 import argparse
@@ -26,7 +28,8 @@ from paper_1212_2287_b200 import distributed as D  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--mode", default="instance", choices=["instance", "tree-reduce", "tree-pipeline"])
+    ap.add_argument("--mode", default="instance", choices=["instance", "tree-reduce", "tree-pipeline",
+                                                             "tree-p2p"])
     ap.add_argument("--rows", type=int, default=None)
     ap.add_argument("--reps", type=int, default=3)
     a = ap.parse_args()
