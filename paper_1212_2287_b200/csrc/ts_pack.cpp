@@ -258,6 +258,8 @@ extern "C" int ts_pack_ex(const ts_model_desc *d, int device, int flags, ts_mode
     if (prev_dev >= 0) cudaSetDevice(prev_dev);
     const int fw = split_fid_width(F);
 
+    // TS_FORCE_CSTREAM: pack complete trees as kCStream too (tests / A/B only)
+    const bool force_cs = getenv("TS_FORCE_CSTREAM") != nullptr;
     std::vector<TreeShape> shapes(T);
     std::vector<int> layout(T);
     int64_t sum_depth = 0, entries = 0;
@@ -271,7 +273,6 @@ extern "C" int ts_pack_ex(const ts_model_desc *d, int device, int flags, ts_mode
         if (rc) return rc;
         const TreeShape &s = shapes[t];
         const int64_t nn = (int64_t)s.bfs.size();
-        static const bool force_cs = getenv("TS_FORCE_CSTREAM") != nullptr;  // A/B only
         if ((s.complete && !force_cs) || !compact_ok_f || nn > 65535) {
             layout[t] = split_ok[s.depth] ? kSplit : kComplete;
             n_complete++;

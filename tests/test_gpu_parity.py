@@ -347,3 +347,15 @@ def test_small_batch_tree_split(n, split, monkeypatch):
     s, o = ref.score(x, threads=4, with_ordinals=True)
     assert np.array_equal(ev.predict_batch(x), s)
     assert np.array_equal(ev.leaf_indices(x), o.astype(np.int64))
+
+
+@pytest.mark.parametrize("name", ["complete_d6", "ties_counts", "trivia"])
+def test_complete_trees_on_irregular_kernel(name, monkeypatch):
+    """TS_FORCE_CSTREAM packs complete trees as child-index records for the
+    irregular-tree kernel: same scores and predicated ordinals."""
+    monkeypatch.setenv("TS_FORCE_CSTREAM", "1")
+    ens, g = load_golden(name)
+    ev = _ev(ens)
+    assert ev.model.info["compact_trees"] == ev.model.info["num_trees"]
+    assert np.array_equal(ev.predict_batch(g["X"]), g["scores"])
+    assert np.array_equal(ev.leaf_indices(g["X"]), g["ordinals"])
