@@ -359,3 +359,35 @@ def test_complete_trees_on_irregular_kernel(name, monkeypatch):
     assert ev.model.info["compact_trees"] == ev.model.info["num_trees"]
     assert np.array_equal(ev.predict_batch(g["X"]), g["scores"])
     assert np.array_equal(ev.leaf_indices(g["X"]), g["ordinals"])
+
+
+@pytest.mark.parametrize("n", [64, 1000, 40000])
+def test_scoring_captured_in_cuda_graph(n):
+    """ts_score is stream-ordered and allocation-free on the host side, so a
+    serving loop can capture it once in a CUDA graph and replay it (the
+    small-batch tree split's scratch comes from a stream-ordered pool, which
+    graphs capture as memory nodes)."""
+    import torch
+    from paper_1212_2287_b200.synth import complete_flat
+    rng = np.random.default_rng(n)
+    T, d, F = 400, 8, 64
+    n_int = (1 << d) - 1
+    flat = complete_flat(F, d, rng.integers(0, F, (T, n_int)), rng.random((T, n_int)),
+                         rng.standard_normal((T, 1 << d)))
+    ev = _ev(flat)
+    x = torch.from_numpy(rng.random((n, F), dtype=np.float32)).cuda()
+    out = torch.empty(n, dtype=torch.float64, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        ev.score_device(x, out)          # warm-up outside capture (smem attributes)
+    s.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        ev.score_device(x, out)
+    ref = oracle.COracle(flat.arrays())
+    for _ in range(2):
+        x.copy_(torch.from_numpy(rng.random((n, F), dtype=np.float32)))
+        out.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy(), ref.score(x.cpu().numpy(), threads=4))

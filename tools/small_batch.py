@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--trees", type=int, default=100)
     ap.add_argument("--ns", default="1000,10000,100000")
     ap.add_argument("--reps", type=int, default=50)
+    ap.add_argument("--graph", action="store_true", help="replay a captured CUDA graph")
     a = ap.parse_args()
     rng = np.random.default_rng(5)
     d, T, F = a.depth, a.trees, 136
@@ -33,11 +34,18 @@ def main():
         out = torch.empty(n, dtype=torch.float64, device="cuda")
         for _ in range(5):
             ev.score_device(x, out)
+        run = lambda: ev.score_device(x, out)  # noqa: E731
+        if a.graph:
+            st = torch.cuda.Stream()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=st):
+                ev.score_device(x, out)
+            run = g.replay
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         s.record()
         for _ in range(a.reps):
-            ev.score_device(x, out)
+            run()
         e.record()
         torch.cuda.synchronize()
         us = s.elapsed_time(e) * 1e3 / a.reps
