@@ -8,8 +8,8 @@ the native library ``_ts_gpu.so`` (C ABI ``include/treescore_gpu.h``) through
 ``build`` / ``build_gpu`` -> :class:`GpuEvaluator`; there is no CPU fallback.
 """
 
-from .data import (DataFormatError, Dataset, as_feature_vector, fvec_header, read_fvec,
-                   read_fvec_into, write_fvec)
+from .data import (DataFormatError, Dataset, as_feature_vector, fvec_header, read_csv,
+                   read_fvec, read_fvec_into, write_csv, write_fvec)
 from .evaluator import (CoverageReport, GpuEvaluator, GpuModel, StrategyKind, TracedPrediction,
                         build, build_gpu)
 from .model import (DUMMY_FID, DUMMY_THETA, MAX_DEPTH, CompleteTree, DepthLimitError,
@@ -17,7 +17,7 @@ from .model import (DUMMY_FID, DUMMY_THETA, MAX_DEPTH, CompleteTree, DepthLimitE
                     Node, Tree, expand_to_complete, load_flat_model, load_model, parse_model,
                     parse_model_native,
                     reference_predict, save_model, serialize_model, traverse_to_leaf,
-                    tree_stats)
+                    TreeStats, tree_stats)
 from ._lib import NativeLibraryError
 
 __version__ = "0.1.0"
@@ -27,7 +27,8 @@ __all__ = [
     "DUMMY_THETA", "Ensemble", "FlatModel", "GpuEvaluator", "GpuModel", "MAX_DEPTH",
     "ModelError", "ModelSemanticError", "ModelSyntaxError", "NativeLibraryError", "Node",
     "StrategyKind", "Tree", "as_feature_vector", "build", "build_gpu", "expand_to_complete",
-    "fvec_header", "load_flat_model", "load_model", "parse_model", "parse_model_native", "read_fvec", "read_fvec_into",
-    "reference_predict", "save_model", "serialize_model", "traverse_to_leaf", "tree_stats",
-    "write_fvec",
+    "fvec_header", "load_flat_model", "load_model", "parse_model", "parse_model_native",
+    "read_csv", "read_fvec", "read_fvec_into",
+    "reference_predict", "save_model", "serialize_model", "traverse_to_leaf", "TreeStats", "tree_stats",
+    "write_csv", "write_fvec",
 ]

@@ -461,11 +461,19 @@ def _as_tree(obj) -> Tree:
     raise ModelSemanticError("tree entry must be a Tree or a Node")
 
 
-def tree_stats(ensemble: Ensemble):
-    """(avg_depth, max_depth, avg_leaves) as in ref ``model.py:236-244``."""
+class TreeStats(NamedTuple):
+    """Depth/leaf statistics of an ensemble (ref ``model.py:229-233``)."""
+
+    avg_depth: float
+    max_depth: int
+    avg_leaves: float
+
+
+def tree_stats(ensemble: Ensemble) -> TreeStats:
+    """Averaged over the ensemble's trees, as ref ``model.py:236-244``."""
     depths = [t.depth for t, _ in ensemble.trees]
     leaves = [t.leaf_count for t, _ in ensemble.trees]
-    return (sum(depths) / len(depths), max(depths), sum(leaves) / len(leaves))
+    return TreeStats(sum(depths) / len(depths), max(depths), sum(leaves) / len(leaves))
 
 
 # ---------------------------------------------------------------------------

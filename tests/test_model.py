@@ -65,7 +65,8 @@ def test_node_narrowing_and_validation():
 def test_tree_stats_and_ensemble_checks():
     t = chain_tree(2)
     assert (t.depth, t.leaf_count, t.node_count) == (2, 3, 5)
-    assert tree_stats(Ensemble(8, [chain_tree(2), chain_tree(4)]))[:2] == (3.0, 4)
+    st = tree_stats(Ensemble(8, [chain_tree(2), chain_tree(4)]))
+    assert st[:2] == (3.0, 4) and st.avg_depth == 3.0 and st.max_depth == 4
     tree = Tree(Node.internal(5, 0.5, Node.leaf(0.0), Node.leaf(1.0)))
     Ensemble(6, [tree])
     with pytest.raises(ModelSemanticError):
