@@ -11,7 +11,7 @@ the native library ``_ts_gpu.so`` (C ABI ``include/treescore_gpu.h``) through
 from .data import (DataFormatError, Dataset, as_feature_vector, fvec_header, read_csv,
                    read_fvec, read_fvec_into, write_csv, write_fvec)
 from .evaluator import (CoverageReport, GpuEvaluator, GpuModel, StrategyKind, TracedPrediction,
-                        build, build_gpu)
+                        build, build_gpu, measure_feature_coverage, predict_ensemble_traced)
 from .model import (DUMMY_FID, DUMMY_THETA, MAX_DEPTH, CompleteTree, DepthLimitError,
                     Ensemble, FlatModel, ModelError, ModelSemanticError, ModelSyntaxError,
                     Node, Tree, expand_to_complete, load_flat_model, load_model, parse_model,
@@ -27,7 +27,7 @@ __all__ = [
     "DUMMY_THETA", "Ensemble", "FlatModel", "GpuEvaluator", "GpuModel", "MAX_DEPTH",
     "ModelError", "ModelSemanticError", "ModelSyntaxError", "NativeLibraryError", "Node",
     "StrategyKind", "Tree", "as_feature_vector", "build", "build_gpu", "expand_to_complete",
-    "fvec_header", "load_flat_model", "load_model", "parse_model", "parse_model_native",
+    "fvec_header", "load_flat_model", "measure_feature_coverage", "predict_ensemble_traced", "load_model", "parse_model", "parse_model_native",
     "read_csv", "read_fvec", "read_fvec_into",
     "reference_predict", "save_model", "serialize_model", "traverse_to_leaf", "TreeStats", "tree_stats",
     "write_csv", "write_fvec",

@@ -495,3 +495,19 @@ def build(ensemble, kind=StrategyKind.GPU_VPREDICATED, batch_size: int | None = 
     """``build`` with the reference's argument meaning and errors (ref :565-585)."""
     kind = StrategyKind(kind)  # ValueError for unknown kinds, as in the reference
     return build_gpu(ensemble, batch_size, device)
+
+
+def predict_ensemble_traced(ensemble, x) -> TracedPrediction:
+    """Drop-in for ref ``evaluators.py:599-620`` on the GPU tracer (``ts_trace``):
+    the score, the union of feature ids on every tree's logical root-to-leaf
+    path, and each tree's left-to-right leaf ordinal.  Packs the model per
+    call; keep a ``build_gpu(ensemble, trace=True)`` evaluator for repeated
+    use."""
+    return build_gpu(ensemble, trace=True).predict_traced(x)
+
+
+def measure_feature_coverage(ensemble, data) -> CoverageReport:
+    """Drop-in for ref ``bench.py:412-427``: mean and population variance of
+    the fraction of features each instance's traversals examined, traced on
+    the GPU for the whole dataset in one launch."""
+    return build_gpu(ensemble, trace=True).feature_coverage(data)

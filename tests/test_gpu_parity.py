@@ -221,6 +221,11 @@ def test_traced_prediction_and_coverage(name):
     tp = ev.predict_traced(g["X"][0])
     assert tp.score == g["scores"][0]
     assert tp.visited_leaves == tuple(g["trace_leaves"][:, 0].tolist())
+    # the reference's module-level names, backed by the same tracer
+    from paper_1212_2287_b200 import Dataset, measure_feature_coverage, predict_ensemble_traced
+    assert predict_ensemble_traced(ens, g["X"][0]) == tp
+    cov2 = measure_feature_coverage(ens, Dataset(g["X"]))
+    assert (cov2.mean_fraction, cov2.variance) == (g["coverage"][0], g["coverage"][1])
 
 
 def test_predict_fvec_streams_files(tmp_path):
