@@ -10,7 +10,7 @@ the native library ``_ts_gpu.so`` (C ABI ``include/treescore_gpu.h``) through
 
 from .data import (DataFormatError, Dataset, as_feature_vector, fvec_header, read_csv,
                    read_fvec, read_fvec_into, write_csv, write_fvec)
-from .evaluator import (CoverageReport, GpuEvaluator, GpuModel, StrategyKind, TracedPrediction,
+from .evaluator import (ALL_STRATEGIES, CoverageReport, GpuEvaluator, GpuModel, StrategyKind, TracedPrediction,
                         build, build_gpu, measure_feature_coverage, predict_ensemble_traced)
 from .model import (DUMMY_FID, DUMMY_THETA, MAX_DEPTH, CompleteTree, DepthLimitError,
                     Ensemble, FlatModel, ModelError, ModelSemanticError, ModelSyntaxError,
@@ -23,7 +23,7 @@ from ._lib import NativeLibraryError
 __version__ = "0.1.0"
 
 __all__ = [
-    "CompleteTree", "CoverageReport", "TracedPrediction", "DataFormatError", "Dataset", "DepthLimitError", "DUMMY_FID",
+    "ALL_STRATEGIES",    "CompleteTree", "CoverageReport", "TracedPrediction", "DataFormatError", "Dataset", "DepthLimitError", "DUMMY_FID",
     "DUMMY_THETA", "Ensemble", "FlatModel", "GpuEvaluator", "GpuModel", "MAX_DEPTH",
     "ModelError", "ModelSemanticError", "ModelSyntaxError", "NativeLibraryError", "Node",
     "StrategyKind", "Tree", "as_feature_vector", "build", "build_gpu", "expand_to_complete",

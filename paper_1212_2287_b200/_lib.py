@@ -99,7 +99,7 @@ def load(build_if_missing: bool = True):
             return _lib
         if not os.path.exists(SO_PATH) and build_if_missing:
             try:
-                from .build import build
+                from ._build import build
                 build()
             except Exception as exc:  # noqa: BLE001 - surfaced below
                 raise NativeLibraryError(f"{SO_PATH} missing and build failed: {exc}") from exc

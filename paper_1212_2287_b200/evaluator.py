@@ -2,10 +2,11 @@
 
 Mirrors ref ``treescore/evaluators.py``:
 
-* ``build(ensemble, kind, batch_size=None)`` (ref :565-585) -- here the kinds
-  are the GPU strategies; ``build_gpu`` is the direct constructor, the way
-  the reference builds its native strategy through ``build_generated``
-  (ref codegen.py:247-253) because ``StrategyKind`` is closed.
+* ``build(ensemble, kind, batch_size=None)`` (ref :565-585) -- accepts the
+  reference's kind names with its argument checks and serves them all with
+  the GPU evaluator; ``build_gpu`` is the direct constructor, the way the
+  reference builds its native strategy through ``build_generated``
+  (ref codegen.py:247-253).
 * ``Evaluator.predict(x)`` / ``predict_batch(data)`` / ``_predict_into``
   (ref :187-231) with the same ``ValueError`` messages for shape mismatch
   (ref :204-220); ``stored_node_count`` (ref :197-200) counts complete-table
@@ -33,12 +34,24 @@ from .model import DepthLimitError, Ensemble, FlatModel, ModelSemanticError
 
 
 class StrategyKind(enum.Enum):
-    """GPU strategies (the reference's enum is closed, ref evaluators.py:56-68)."""
+    """The reference's strategy names (ref evaluators.py:56-68) plus the GPU
+    one.  Every strategy scores bit-identically by the reference's contract,
+    so ``build`` serves all accepted kinds with the GPU evaluator; the kind
+    only selects the reference's argument checks."""
 
+    HEAP_LINKED = "heap_linked"
+    COMPACT_LINKED = "compact_linked"
+    CONTIGUOUS = "contiguous"
+    PREDICATED = "predicated"
+    VPREDICATED = "vpredicated"
+    GENERATED = "generated"
     GPU_VPREDICATED = "gpu_vpredicated"
 
     def __str__(self):
         return self.value
+
+
+ALL_STRATEGIES = tuple(StrategyKind)  # ref evaluators.py:69
 
 
 def _torch():
@@ -492,8 +505,23 @@ def build_gpu(ensemble, batch_size: int | None = None, device: int | None = None
 
 def build(ensemble, kind=StrategyKind.GPU_VPREDICATED, batch_size: int | None = None,
           device: int | None = None) -> GpuEvaluator:
-    """``build`` with the reference's argument meaning and errors (ref :565-585)."""
+    """``build`` with the reference's argument meaning and errors (ref :565-585):
+    unknown kinds raise ``ValueError``; ``generated`` is compiled C in the
+    reference (``ValueError`` here as there); ``vpredicated`` requires a
+    ``batch_size`` and the other reference kinds reject one.  Any accepted
+    kind returns the GPU evaluator (the reference guarantees bit-identical
+    scores across strategies), so ``build(ens, "vpredicated", 16)`` works
+    unchanged.  One difference: trees deeper than ``MAX_DEPTH`` raise
+    ``DepthLimitError`` for the linked kinds too (the GPU walk is predicated)."""
     kind = StrategyKind(kind)  # ValueError for unknown kinds, as in the reference
+    if kind is StrategyKind.GENERATED:
+        raise ValueError(
+            "generated evaluators are compiled; use treescore.codegen.build_generated")
+    if kind is StrategyKind.VPREDICATED and batch_size is None:
+        raise ValueError("vpredicated requires a batch_size (v >= 1)")
+    if kind not in (StrategyKind.VPREDICATED, StrategyKind.GPU_VPREDICATED) \
+            and batch_size is not None:
+        raise ValueError(f"batch_size does not apply to {kind.value}")
     return build_gpu(ensemble, batch_size, device)
 
 

@@ -396,3 +396,21 @@ def test_scoring_captured_in_cuda_graph(n):
         g.replay()
         torch.cuda.synchronize()
         assert np.array_equal(out.cpu().numpy(), ref.score(x.cpu().numpy(), threads=4))
+
+
+def test_build_accepts_reference_kinds():
+    # ref evaluators.py:565-585 argument checks; every kind scores the same
+    from paper_1212_2287_b200 import StrategyKind, build
+    ens, g = load_golden("mixed")
+    for kind, v in (("vpredicated", 16), ("predicated", None), ("heap_linked", None),
+                    ("compact_linked", None), ("contiguous", None),
+                    (StrategyKind.GPU_VPREDICATED, None)):
+        assert np.array_equal(build(ens, kind, v).predict_batch(g["X"]), g["scores"])
+    with pytest.raises(ValueError, match="requires a batch_size"):
+        build(ens, "vpredicated")
+    with pytest.raises(ValueError, match="does not apply"):
+        build(ens, "heap_linked", 4)
+    with pytest.raises(ValueError, match="compiled"):
+        build(ens, "generated")
+    with pytest.raises(ValueError):
+        build(ens, "no_such_kind")

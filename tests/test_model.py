@@ -150,7 +150,7 @@ def test_adopts_reference_ensemble_objects():
 
 def _native():
     from paper_1212_2287_b200 import parse_model_native
-    from paper_1212_2287_b200.build import build
+    from paper_1212_2287_b200._build import build
     build()
     return parse_model_native
 

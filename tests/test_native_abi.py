@@ -5,7 +5,7 @@ import os
 import re
 
 from paper_1212_2287_b200 import _lib
-from paper_1212_2287_b200.build import build
+from paper_1212_2287_b200._build import build
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -54,3 +54,11 @@ def test_pack_rejects_bad_models_without_gpu():
     val[0] = np.inf
     assert lib.ts_pack(ctypes.byref(desc), 0, ctypes.byref(h)) == _lib.TS_ERR_INVALID
     assert "finite" in _lib.last_error()
+
+
+def test_package_build_is_the_reference_build_function():
+    # the native-library builder is a private module, so importing it never
+    # rebinds the package attribute `build` (the reference's build(ensemble, kind))
+    import paper_1212_2287_b200 as pkg
+    import paper_1212_2287_b200._build  # noqa: F401
+    assert callable(pkg.build) and pkg.build.__module__ == "paper_1212_2287_b200.evaluator"

@@ -4,7 +4,7 @@
 # range-checked and traps) and run the GPU parity suite and all configs on it.
 # Usage on the GPU box: bash tools/debug_check.sh   (build it here first with
 #   TS_NVCC_EXTRA=-DTS_DEBUG TS_GPU_SO=$PWD/paper_1212_2287_b200/_ts_gpu_debug.so \
-#   python paper_1212_2287_b200/build.py --force)
+#   python paper_1212_2287_b200/_build.py --force)
 set -e
 export TS_GPU_SO=$PWD/paper_1212_2287_b200/_ts_gpu_debug.so
 python -m pytest tests -m gpu -x -q
