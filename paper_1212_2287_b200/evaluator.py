@@ -119,6 +119,7 @@ class GpuModel:
         self.info = info.as_dict()
         self.num_features = int(flat.num_features)
         self.num_trees = int(flat.num_trees)
+        self.node_count = int(flat.tree_off[-1])  # logical nodes (internal + leaves)
 
     def score(self, x, out=None, ordinals=None, status=None, stream=None, accumulate=False):
         """Enqueue scoring of a CUDA float32 ``[n, f]`` tensor (row stride >= f).
@@ -295,7 +296,9 @@ class GpuEvaluator:
     kind = StrategyKind.GPU_VPREDICATED
 
     def __init__(self, ensemble, batch_size: int | None = None, device: int | None = None,
-                 trace: bool = False):
+                 trace: bool = False, kind: StrategyKind | None = None):
+        if kind is not None:
+            self.kind = StrategyKind(kind)
         if batch_size is not None:
             batch_size = int(batch_size)
             if batch_size < 1:
@@ -339,6 +342,12 @@ class GpuEvaluator:
 
     @property
     def stored_node_count(self) -> int:
+        """As the reference's kind would count it (ref evaluators.py:297-474):
+        the trees' own nodes for the linked / contiguous kinds, complete-table
+        slots (2^(d+1) - 1 per tree) for the predicated ones."""
+        if self.kind in (StrategyKind.HEAP_LINKED, StrategyKind.COMPACT_LINKED,
+                         StrategyKind.CONTIGUOUS):
+            return self.model.node_count
         return int(self.model.info["table_entries"])
 
     # -- GPU-native extras ---------------------------------------------------------
@@ -495,12 +504,12 @@ class GpuEvaluator:
 
 
 def build_gpu(ensemble, batch_size: int | None = None, device: int | None = None,
-              trace: bool = False) -> GpuEvaluator:
+              trace: bool = False, kind: StrategyKind | None = None) -> GpuEvaluator:
     """Pack ``ensemble`` (Ensemble, FlatModel or reference treescore Ensemble).
     ``trace=True`` also uploads the logical trees for traced prediction."""
     if not isinstance(ensemble, (Ensemble, FlatModel)) and hasattr(ensemble, "trees"):
         ensemble = Ensemble.from_reference(ensemble)
-    return GpuEvaluator(ensemble, batch_size, device, trace=trace)
+    return GpuEvaluator(ensemble, batch_size, device, trace=trace, kind=kind)
 
 
 def build(ensemble, kind=StrategyKind.GPU_VPREDICATED, batch_size: int | None = None,
@@ -522,7 +531,7 @@ def build(ensemble, kind=StrategyKind.GPU_VPREDICATED, batch_size: int | None = 
     if kind not in (StrategyKind.VPREDICATED, StrategyKind.GPU_VPREDICATED) \
             and batch_size is not None:
         raise ValueError(f"batch_size does not apply to {kind.value}")
-    return build_gpu(ensemble, batch_size, device)
+    return build_gpu(ensemble, batch_size, device, kind=kind)
 
 
 def predict_ensemble_traced(ensemble, x) -> TracedPrediction:

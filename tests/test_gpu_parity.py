@@ -406,6 +406,16 @@ def test_build_accepts_reference_kinds():
                     ("compact_linked", None), ("contiguous", None),
                     (StrategyKind.GPU_VPREDICATED, None)):
         assert np.array_equal(build(ens, kind, v).predict_batch(g["X"]), g["scores"])
+    # ref tests/test_evaluators.py:78-82, 238-262: kind and stored_node_count
+    from paper_1212_2287_b200 import Ensemble, Node, Tree
+    tree = Tree(Node.internal(0, 0.5, Node.leaf(1.0),
+                              Node.internal(1, 0.25, Node.leaf(2.0), Node.leaf(3.0))))
+    small = Ensemble(2, [tree])
+    for kind in ("heap_linked", "compact_linked", "contiguous"):
+        ev = build(small, kind)
+        assert ev.kind is StrategyKind(kind) and ev.stored_node_count == 5
+    assert build(small, "predicated").stored_node_count == 7
+    assert build(small, "vpredicated", 8).stored_node_count == 7
     with pytest.raises(ValueError, match="requires a batch_size"):
         build(ens, "vpredicated")
     with pytest.raises(ValueError, match="does not apply"):
