@@ -424,3 +424,61 @@ def test_build_accepts_reference_kinds():
         build(ens, "generated")
     with pytest.raises(ValueError):
         build(ens, "no_such_kind")
+
+
+def _rand_unbalanced(rng, max_depth, f, prune=0.35):
+    from paper_1212_2287_b200 import Node, Tree
+
+    def build_node(level):
+        if level == max_depth or (level > 0 and rng.random() < prune):
+            return Node.leaf(rng.random())
+        return Node.internal(int(rng.integers(f)), rng.random(), build_node(level + 1),
+                             build_node(level + 1))
+    return Tree(build_node(0))
+
+
+def _rand_complete(rng, depth, f):
+    from paper_1212_2287_b200 import Node, Tree
+
+    def build_node(level):
+        if level == depth:
+            return Node.leaf(rng.standard_normal())
+        return Node.internal(int(rng.integers(f)), rng.random(), build_node(level + 1),
+                             build_node(level + 1))
+    return Tree(build_node(0))
+
+
+def test_acceptance_cross_strategy_schedule():
+    """The reference's acceptance criterion 1 (ref tests/test_acceptance.py:
+    83-125) on the GPU: 200 ensembles over f = 32/128/512 with its schedule
+    of shapes (a complete tree of the slot's depth first, then balanced and
+    pruned trees; a single d=11 / d=9 tree, 50 d=2 trees, 2 d=7 trees in the
+    special slots), weights U(0.5, 1.5), 100 vectors each -- bit-exact
+    against the pinned C oracle, scores and ordinals."""
+    from paper_1212_2287_b200 import Ensemble
+    rng = np.random.default_rng(101)
+    for i in range(200):
+        f = (32, 128, 512)[i % 3]
+        slot = i % 40
+        if slot == 7:
+            depth, trees = 11, 1
+        elif slot == 15:
+            depth, trees = 9, 1
+        elif slot == 23:
+            depth, trees = 2, 50
+        elif slot == 31:
+            depth, trees = 7, 2
+        else:
+            depth = int(rng.integers(0, 7))
+            trees = min(1 + int(min(rng.geometric(0.35), 49)), max(1, 512 >> depth))
+        ts = [(_rand_complete(rng, depth, f), float(rng.uniform(0.5, 1.5)))]
+        for t in range(1, trees):
+            tree = _rand_complete(rng, int(rng.integers(0, depth + 1)), f) if t % 2 == 0 \
+                else _rand_unbalanced(rng, depth, f)
+            ts.append((tree, float(rng.uniform(0.5, 1.5))))
+        ens = Ensemble(f, ts)
+        X = rng.random((100, f), dtype=np.float32)
+        s, o = oracle.COracle(ens.flat().arrays()).score(X, threads=2, with_ordinals=True)
+        ev = _ev(ens)
+        assert np.array_equal(ev.predict_batch(X), s), (i, depth, f, trees)
+        assert np.array_equal(ev.leaf_indices(X), o.astype(np.int64)), (i, depth, f, trees)
