@@ -482,3 +482,57 @@ def test_acceptance_cross_strategy_schedule():
         ev = _ev(ens)
         assert np.array_equal(ev.predict_batch(X), s), (i, depth, f, trees)
         assert np.array_equal(ev.leaf_indices(X), o.astype(np.int64)), (i, depth, f, trees)
+
+
+@pytest.mark.parametrize("depth", [1, 2, 3, 5, 8])
+def test_acceptance_per_leaf_probes(depth):
+    """The reference's acceptance criterion 2 (ref tests/test_acceptance.py:
+    132-161) on the GPU: for a complete tree, one probe vector per reachable
+    leaf (built from the path's bounds: right turns need x >= theta, left
+    turns x < theta) must come back with that leaf's predicated ordinal."""
+    from paper_1212_2287_b200.synth import complete_flat
+    rng = np.random.default_rng(depth + 100)
+    f = 16
+    n_int = (1 << depth) - 1
+    fids = rng.integers(0, f, n_int)
+    thr = rng.random(n_int).astype(np.float32)
+    flat = complete_flat(f, depth, fids[None], thr[None], np.arange(1 << depth)[None] * 1.0)
+    probes, want = [], []
+    for leaf in range(1 << depth):
+        lo = np.full(f, -1.0, np.float64)
+        hi = np.full(f, 2.0, np.float64)
+        node = 0
+        for level in range(depth):
+            right = (leaf >> (depth - 1 - level)) & 1
+            fid, t = fids[node], float(thr[node])
+            if right:
+                lo[fid] = max(lo[fid], t)
+            else:
+                hi[fid] = min(hi[fid], t)
+            node = 2 * node + 1 + right
+        if np.all(lo < hi):
+            x = np.where(lo > -1.0, lo, np.minimum(hi, 0.0) - 0.5).astype(np.float32)
+            probes.append(x)   # x = lo exactly satisfies x >= theta; below hi otherwise
+            want.append(leaf)
+    assert len(want) * 2 > (1 << depth)   # most leaves are reachable (140/256 at d=8)
+    X = np.stack(probes)
+    ev = _ev(flat)
+    got = ev.leaf_indices(X)[0]
+    assert got.tolist() == want
+    assert np.array_equal(ev.predict_batch(X), np.array(want, np.float64))
+
+
+@pytest.mark.parametrize("depth", [9, 11])
+def test_acceptance_random_probes_deep(depth):
+    # ref tests/test_acceptance.py:149-158: 10k random probes at d = 9 and 11
+    from paper_1212_2287_b200.synth import complete_flat
+    rng = np.random.default_rng(202 + depth)
+    f = 32
+    n_int = (1 << depth) - 1
+    flat = complete_flat(f, depth, rng.integers(0, f, (1, n_int)), rng.random((1, n_int)),
+                         rng.standard_normal((1, 1 << depth)))
+    X = rng.random((10000, f), dtype=np.float32)
+    s, o = oracle.COracle(flat.arrays()).score(X, threads=4, with_ordinals=True)
+    ev = _ev(flat)
+    assert np.array_equal(ev.leaf_indices(X), o.astype(np.int64))
+    assert np.array_equal(ev.predict_batch(X), s)
