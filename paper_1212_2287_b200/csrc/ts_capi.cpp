@@ -16,7 +16,7 @@ namespace ts {
 
 static thread_local std::string g_err;
 static std::atomic<long long> g_launches{0};
-static int g_kernel_path = 0;  // ts_set_kernel_path
+static std::atomic<int> g_kernel_path{0};  // ts_set_kernel_path
 
 void set_error(const std::string &msg) { g_err = msg; }
 
@@ -34,7 +34,7 @@ int cuda_fail(cudaError_t err, const char *what) {
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
-int kernel_path() { return g_kernel_path; }
+int kernel_path() { return g_kernel_path.load(std::memory_order_relaxed); }
 
 const DevAttrs &dev_attrs(int device) {
     static DevAttrs cache[64];
@@ -234,7 +234,13 @@ extern "C" int ts_pipe_alloc(int device, int64_t n, double **sums, uint32_t **fl
         memcpy(sums_handle64, &hs, sizeof hs);
     if (e == cudaSuccess && flags_handle64 && (e = cudaIpcGetMemHandle(&hf, *flags)) == cudaSuccess)
         memcpy(flags_handle64, &hf, sizeof hf);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle");
+    if (e != cudaSuccess) {
+        cudaFree(*sums);
+        cudaFree(*flags);
+        *sums = nullptr;
+        *flags = nullptr;
+        return cuda_fail(e, "cudaIpcGetMemHandle");
+    }
     return TS_OK;
 }
 
@@ -303,6 +309,13 @@ extern "C" int ts_score_host(const ts_model *mc, const float *x, int64_t n, int6
     // Full chunks, then halving pieces over the last two chunks' worth of
     // rows, so the part not overlapped with a copy (the last piece's kernel
     // and D2H) is small.
+    // On a mid-pipeline error the copies already queued may still read x or
+    // write out: drain both streams before handing the buffers back.
+    auto drain = [&s](int code) {
+        cudaStreamSynchronize(s.copy);
+        cudaStreamSynchronize(s.compute);
+        return code;
+    };
     int k = 0;
     int64_t rows = 0;
     for (int64_t r0 = 0; r0 < n; r0 += rows, k ^= 1) {
@@ -315,14 +328,14 @@ extern "C" int ts_score_host(const ts_model *mc, const float *x, int64_t n, int6
                                  s.copy)) ||
             (e = cudaEventRecord(s.copied[k], s.copy)) ||
             (e = cudaStreamWaitEvent(s.compute, s.copied[k], 0)))
-            return cuda_fail(e, "host pipeline (H2D)");
+            return drain(cuda_fail(e, "host pipeline (H2D)"));
         double *dout = s.out + k * chunk;
         rc = score_device(m, s.x[k], rows, f, f, dout, nullptr, 0, s.status, s.compute);
-        if (rc) return rc;
+        if (rc) return drain(rc);
         if ((e = cudaEventRecord(s.consumed[k], s.compute)) ||
             (e = cudaMemcpyAsync(out + r0, dout, rows * sizeof(double), cudaMemcpyDeviceToHost,
                                  s.compute)))
-            return cuda_fail(e, "host pipeline (D2H)");
+            return drain(cuda_fail(e, "host pipeline (D2H)"));
     }
     int32_t flag = 0;
     if ((e = cudaMemcpyAsync(&flag, s.status, sizeof(int32_t), cudaMemcpyDeviceToHost,
