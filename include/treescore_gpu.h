@@ -168,6 +168,22 @@ void ts_pipe_free(double *sums, uint32_t *flags);
 int ts_ipc_open(const void *handle64, void **dev_ptr);
 void ts_ipc_close(void *dev_ptr);
 
+/* Tree-shard partial scores combined by ONE NCCL f64 sum-reduce to `root`
+ * over NVLink / NVSwitch (SURVEY 8(b) ts_reduce_partials; the NCCL
+ * equivalent of the reference's sequential sum is exact to ~1e-16 relative,
+ * not bit-exact -- ts_score_pipe is the bit-exact alternative).  NCCL is
+ * resolved at run time (libnccl.so.2); TS_ERR_UNSUPPORTED without it.
+ *   ts_nccl_get_unique_id: on one rank; broadcast the 128 bytes to the others
+ *   ts_nccl_comm_init:     every rank, device = its GPU
+ *   ts_reduce_partials:    out (valid on root) = sum over ranks of partial[n]
+ * A communicator created by the caller's own NCCL (ncclComm_t) may be
+ * passed as `comm` as well. */
+int ts_nccl_get_unique_id(void *id128);
+int ts_nccl_comm_init(const void *id128, int nranks, int rank, int device, void **comm);
+int ts_reduce_partials(void *comm, const double *partial, double *out, int64_t n, int root,
+                       void *stream);
+int ts_nccl_comm_destroy(void *comm);
+
 /* Host-buffer scoring: same argument meaning as the reference's generated
  * score_batch(x, n, f, out).  Copies x to the device in chunks on two
  * streams (H2D of chunk i+1 overlaps scoring of chunk i), copies the scores

@@ -19,7 +19,7 @@ CSRC = os.path.join(HERE, "csrc")
 SO = os.environ.get("TS_GPU_SO") or os.path.join(HERE, "_ts_gpu.so")
 SOURCES = ["ts_kernels.cu", "ts_stream.cu", "ts_stream_i0.cu", "ts_stream_i1.cu",
            "ts_stream_i2.cu", "ts_stream_i3.cu", "ts_stream_i4.cu", "ts_cstream.cu", "ts_cstream_w8.cu", "ts_cstream_w16.cu", "ts_trace.cu", "ts_synth.cu",
-           "ts_pack.cpp", "ts_parse.cpp", "ts_capi.cpp"]
+           "ts_pack.cpp", "ts_parse.cpp", "ts_capi.cpp", "ts_nccl.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -66,7 +66,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
                                f"{res.stdout}\n{res.stderr}")
         if verbose:
             sys.stderr.write(res.stderr)
-    link = [nvcc(), *ARCH, "-shared", "-o", SO + ".tmp"] + [r[1] for r in results]
+    link = [nvcc(), *ARCH, "-shared", "-o", SO + ".tmp"] + [r[1] for r in results] + ["-ldl"]
     res = subprocess.run(link, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"link failed:\n{' '.join(link)}\n{res.stdout}\n{res.stderr}")

@@ -30,7 +30,8 @@ TS_PACK_TRACE = 1
 EXPORTS = ("ts_pack", "ts_pack_ex", "ts_trace", "ts_model_get_info", "ts_score", "ts_score_ex", "ts_score_host", "ts_free",
            "ts_last_error", "ts_launch_count", "ts_version", "ts_synth_uniform", "ts_set_kernel_path",
            "ts_parse_model", "ts_flat_free", "ts_score_pipe", "ts_pipe_alloc", "ts_pipe_free",
-           "ts_ipc_open", "ts_ipc_close")
+           "ts_ipc_open", "ts_ipc_close", "ts_nccl_get_unique_id", "ts_nccl_comm_init",
+           "ts_reduce_partials", "ts_nccl_comm_destroy")
 
 
 class NativeLibraryError(RuntimeError):
@@ -151,6 +152,11 @@ def load(build_if_missing: bool = True):
         lib.ts_ipc_open.restype = ctypes.c_int
         lib.ts_ipc_close.argtypes = [P]
         lib.ts_ipc_close.restype = None
+        lib.ts_nccl_get_unique_id.argtypes = [P]
+        lib.ts_nccl_comm_init.argtypes = [P, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                          ctypes.POINTER(P)]
+        lib.ts_reduce_partials.argtypes = [P, P, P, I64, ctypes.c_int, P]
+        lib.ts_nccl_comm_destroy.argtypes = [P]
         for name in EXPORTS:
             getattr(lib, name)
         _lib = lib

@@ -211,6 +211,51 @@ class ShardedScorer:
                 b.close()
 
 
+class NcclReducer:
+    """The C ABI's NCCL reduction of tree-shard partials (``ts_reduce_partials``,
+    SURVEY 8(b)): a communicator of its own over the ranks of ``group``, the
+    unique id broadcast from rank 0 on the host."""
+
+    def __init__(self, device: int, group=None):
+        import ctypes
+        import torch.distributed as dist
+        from . import _lib
+        self._lib = lib = _lib.load()
+        self.world, self.rank = dist.get_world_size(group), dist.get_rank(group)
+        uid = ctypes.create_string_buffer(128)
+        if self.rank == 0 and lib.ts_nccl_get_unique_id(uid) != _lib.TS_OK:
+            raise RuntimeError(f"ts_nccl_get_unique_id: {_lib.last_error()}")
+        box = [uid.raw if self.rank == 0 else None]
+        dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0)
+                                   if group is not None else 0, group=group)
+        uid = ctypes.create_string_buffer(box[0], 128)
+        comm = ctypes.c_void_p()
+        if lib.ts_nccl_comm_init(uid, self.world, self.rank, int(device),
+                                 ctypes.byref(comm)) != _lib.TS_OK:
+            raise RuntimeError(f"ts_nccl_comm_init: {_lib.last_error()}")
+        self.comm = comm
+
+    def reduce(self, partial, out=None, root: int = 0):
+        """``out`` (valid on ``root``) = sum over ranks of the f64 ``partial``."""
+        import ctypes
+        import torch
+        from . import _lib
+        if out is None:
+            out = torch.empty_like(partial)
+        rc = self._lib.ts_reduce_partials(self.comm, ctypes.c_void_p(partial.data_ptr()),
+                                          ctypes.c_void_p(out.data_ptr()), partial.numel(),
+                                          root, ctypes.c_void_p(
+                                              torch.cuda.current_stream(partial.device).cuda_stream))
+        if rc != _lib.TS_OK:
+            raise RuntimeError(f"ts_reduce_partials: {_lib.last_error()}")
+        return out
+
+    def close(self):
+        if getattr(self, "comm", None) is not None and self.comm.value:
+            self._lib.ts_nccl_comm_destroy(self.comm)
+            self.comm = None
+
+
 def run_sharded(mode: str, flat: FlatModel, x_local, n_total: int, **kw):
     """One-shot :class:`ShardedScorer`; returns ``(plan, scores)``."""
     sc = ShardedScorer(mode, flat, n_total, **kw)

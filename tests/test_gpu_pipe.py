@@ -131,3 +131,35 @@ def test_pipe_two_processes_cuda_ipc():
     ref = oracle.COracle(flat.arrays()).score(x, threads=4)
     assert np.array_equal(res[1][0], ref)
     assert np.array_equal(res[1][1], ref)
+
+
+def _reduce_worker(rank, world, port, q):
+    try:
+        import torch
+        import torch.distributed as dist
+        from paper_1212_2287_b200.distributed import NcclReducer
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        red = NcclReducer(0)
+        part = torch.arange(1000, dtype=torch.float64, device="cuda") * 0.5
+        out = red.reduce(part)
+        torch.cuda.synchronize()
+        red.close()
+        dist.destroy_process_group()
+        q.put((rank, out.cpu().numpy()))
+    except Exception as e:  # noqa: BLE001
+        q.put((rank, repr(e)))
+
+
+def test_native_nccl_reduce_world1():
+    """ts_reduce_partials (the C ABI's NCCL f64 sum-reduce) through its own
+    communicator; one GPU, so world size 1 (the sum is the partial itself)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_reduce_worker, args=(0, 1, _free_port(), q))
+    p.start()
+    rank, res = q.get(timeout=300)
+    p.join(timeout=60)
+    assert not isinstance(res, str), res
+    assert np.array_equal(res, np.arange(1000) * 0.5)
