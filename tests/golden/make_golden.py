@@ -204,6 +204,30 @@ def main():
     X[rng.random(X.shape) < 0.4] = 0.0
     save("wide_irregular", ts.Ensemble(700, trees), X)
 
+    # 10. config-1 shape in miniature: F=136 with uniform, lognormal and
+    #     integer-count columns, complete depth-8 trees whose thresholds are
+    #     values of the split column in a sample of rows (exact ties occur)
+    rng = np.random.default_rng(10)
+    kinds = rng.permutation(np.array([0] * 95 + [1] * 27 + [2] * 14))
+    X = np.empty((512, 136), np.float32)
+    for c, kind in enumerate(kinds):
+        if kind == 0:
+            X[:, c] = rng.random(512, dtype=np.float32)
+        elif kind == 1:
+            X[:, c] = rng.lognormal(0.0, 1.0, 512).astype(np.float32)
+        else:
+            X[:, c] = rng.integers(0, 51, 512).astype(np.float32)
+    trees = []
+    for _ in range(12):
+        def build(level):
+            if level == 8:
+                return ts.Node.leaf(0.1 * rng.standard_normal())
+            fid = int(rng.integers(136))
+            return ts.Node.internal(fid, float(X[int(rng.integers(512)), fid]),
+                                    build(level + 1), build(level + 1))
+        trees.append(ts.Tree(build(0)))
+    save("cfg1_ties_d8", ts.Ensemble(136, trees), X)
+
 
 if __name__ == "__main__":
     main()
