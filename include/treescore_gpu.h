@@ -96,8 +96,15 @@ typedef struct {
 int ts_pack(const ts_model_desc *desc, int device, ts_model **out);
 
 /* ts_pack with options: TS_PACK_TRACE also uploads the logical trees for
- * ts_trace (16 bytes per node). */
+ * ts_trace (16 bytes per node).  TS_PACK_ANY_DEPTH accepts trees deeper than
+ * TS_MAX_DEPTH (up to TS_MAX_LINKED_DEPTH levels, <= 65535 nodes each), as the
+ * reference's linked strategies do (ref evaluators.py: heap/compact linked,
+ * contiguous): they are walked from their own child-index records; such a
+ * model scores normally but refuses predicated ordinals (ord_out) with
+ * TS_ERR_DEPTH, since no complete table exists for them. */
 #define TS_PACK_TRACE 1
+#define TS_PACK_ANY_DEPTH 2
+#define TS_MAX_LINKED_DEPTH 31
 int ts_pack_ex(const ts_model_desc *desc, int device, int flags, ts_model **out);
 
 int ts_model_get_info(const ts_model *model, ts_model_info *info);

@@ -25,6 +25,7 @@ TS_ERR_NOMEM = 6
 TS_ERR_UNSUPPORTED = 7
 TS_ERR_SYNTAX = 8
 TS_PACK_TRACE = 1
+TS_PACK_ANY_DEPTH = 2
 
 # Every symbol include/treescore_gpu.h declares (checked by the CPU tests).
 EXPORTS = ("ts_pack", "ts_pack_ex", "ts_trace", "ts_model_get_info", "ts_score", "ts_score_ex", "ts_score_host", "ts_free",

@@ -170,6 +170,8 @@ extern "C" int ts_score(const ts_model *m, const float *x, int64_t n, int64_t f,
     int rc = check_args(m, x, n, f, ld, out);
     if (rc) return rc;
     if (ord_out && ld_ord < n) return fail(TS_ERR_SHAPE, "ld_ord must be >= n");
+    if (ord_out && m->info.max_depth > TS_MAX_DEPTH)
+        return fail(TS_ERR_DEPTH, "predicated ordinals need trees of depth <= MAX_DEPTH");
     DeviceGuard g(m->device);
     if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
     return score_device(m, x, n, f, ld, out, ord_out, ld_ord, status, (cudaStream_t)stream);
@@ -181,6 +183,8 @@ extern "C" int ts_score_ex(const ts_model *m, const float *x, int64_t n, int64_t
     int rc = check_args(m, x, n, f, ld, out);
     if (rc) return rc;
     if (ord_out && ld_ord < n) return fail(TS_ERR_SHAPE, "ld_ord must be >= n");
+    if (ord_out && m->info.max_depth > TS_MAX_DEPTH)
+        return fail(TS_ERR_DEPTH, "predicated ordinals need trees of depth <= MAX_DEPTH");
     DeviceGuard g(m->device);
     if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
     return score_device(m, x, n, f, ld, out, ord_out, ld_ord, status, (cudaStream_t)stream,

@@ -36,7 +36,7 @@ std::string tree_msg(int t, const char *what) {
 }
 
 // Structure check + depth.  Returns TS_OK or an error code (message set).
-int analyse_tree(const ts_model_desc *d, int t, TreeShape *s) {
+int analyse_tree(const ts_model_desc *d, int t, TreeShape *s, int max_depth) {
     const int64_t o = d->tree_node_offset[t];
     const int64_t n64 = d->tree_node_offset[t + 1] - o;
     if (n64 <= 0) return fail(TS_ERR_INVALID, tree_msg(t, "empty tree block"));
@@ -82,10 +82,10 @@ int analyse_tree(const ts_model_desc *d, int t, TreeShape *s) {
     }
     if ((int32_t)s->bfs.size() != n)
         return fail(TS_ERR_INVALID, tree_msg(t, "node unreachable from the root"));
-    if (depth > TS_MAX_DEPTH) {
+    if (depth > max_depth) {
         char buf[160];
         snprintf(buf, sizeof buf, "tree %d: depth %d exceeds MAX_DEPTH=%d for complete-table "
-                 "layouts", t, depth, TS_MAX_DEPTH);
+                 "layouts", t, depth, max_depth);
         return fail(TS_ERR_DEPTH, buf);
     }
     s->depth = depth;
@@ -269,11 +269,16 @@ extern "C" int ts_pack_ex(const ts_model_desc *d, int device, int flags, ts_mode
         if (!isfinite(d->tree_weight[t]))
             return fail(TS_ERR_INVALID, tree_msg(t, "tree weight must be finite"));
         if (d->tree_weight[t] != 1.0) unit = false;
-        int rc = analyse_tree(d, t, &shapes[t]);
+        int rc = analyse_tree(d, t, &shapes[t],
+                              (flags & TS_PACK_ANY_DEPTH) ? TS_MAX_LINKED_DEPTH : TS_MAX_DEPTH);
         if (rc) return rc;
         const TreeShape &s = shapes[t];
         const int64_t nn = (int64_t)s.bfs.size();
-        if ((s.complete && !force_cs) || !compact_ok_f || nn > 65535) {
+        if (s.depth > TS_MAX_DEPTH && (!compact_ok_f || nn > 65535))
+            return fail(TS_ERR_DEPTH, tree_msg(t, "deeper than MAX_DEPTH and too large for the "
+                                                  "child-index layout"));
+        const bool deep = s.depth > TS_MAX_DEPTH;  // no complete table: child-index records
+        if (!deep && ((s.complete && !force_cs) || !compact_ok_f || nn > 65535)) {
             layout[t] = split_ok[s.depth] ? kSplit : kComplete;
             n_complete++;
         } else {

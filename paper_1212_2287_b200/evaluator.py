@@ -52,6 +52,7 @@ class StrategyKind(enum.Enum):
 
 
 ALL_STRATEGIES = tuple(StrategyKind)  # ref evaluators.py:69
+_LINKED_KINDS = (StrategyKind.HEAP_LINKED, StrategyKind.COMPACT_LINKED, StrategyKind.CONTIGUOUS)
 
 
 def _torch():
@@ -86,7 +87,8 @@ class CoverageReport:
 class GpuModel:
     """Packed device tables of one ensemble on one GPU (``ts_pack``)."""
 
-    def __init__(self, model, device: int | None = None, trace: bool = False):
+    def __init__(self, model, device: int | None = None, trace: bool = False,
+                 any_depth: bool = False):
         torch = _torch()
         if not torch.cuda.is_available():
             raise _lib.NativeLibraryError("no CUDA device: the GPU scorer has no CPU fallback")
@@ -104,7 +106,8 @@ class GpuModel:
         desc = _lib.ModelDesc(int(flat.num_features), int(flat.num_trees),
                               *[a.ctypes.data for a in arrs])
         handle = ctypes.c_void_p()
-        rc = lib.ts_pack_ex(ctypes.byref(desc), self.device, _lib.TS_PACK_TRACE if trace else 0,
+        flags = (_lib.TS_PACK_TRACE if trace else 0) | (_lib.TS_PACK_ANY_DEPTH if any_depth else 0)
+        rc = lib.ts_pack_ex(ctypes.byref(desc), self.device, flags,
                             ctypes.byref(handle))
         if rc == _lib.TS_ERR_DEPTH:
             raise DepthLimitError(_lib.last_error())
@@ -158,6 +161,8 @@ class GpuModel:
                                    ctypes.c_void_p(status.data_ptr()) if status is not None
                                    else None, 1 if accumulate else 0,
                                    ctypes.c_void_p(stream.cuda_stream))
+        if rc == _lib.TS_ERR_DEPTH:
+            raise DepthLimitError(_lib.last_error())
         if rc != _lib.TS_OK:
             raise RuntimeError(f"ts_score failed ({rc}): {_lib.last_error()}")
         return out
@@ -304,7 +309,10 @@ class GpuEvaluator:
             if batch_size < 1:
                 raise ValueError(f"batch_size must be >= 1, got {batch_size}")
         self.batch_size = batch_size
-        self.model = GpuModel(ensemble, device, trace=trace)
+        # the reference's linked kinds walk trees of any depth (no complete
+        # table); so does the GPU packer's child-index layout
+        self.model = GpuModel(ensemble, device, trace=trace,
+                              any_depth=self.kind in _LINKED_KINDS)
         self.num_features = self.model.num_features
         self.num_trees = self.model.num_trees
         self.device = self.model.device
@@ -345,8 +353,7 @@ class GpuEvaluator:
         """As the reference's kind would count it (ref evaluators.py:297-474):
         the trees' own nodes for the linked / contiguous kinds, complete-table
         slots (2^(d+1) - 1 per tree) for the predicated ones."""
-        if self.kind in (StrategyKind.HEAP_LINKED, StrategyKind.COMPACT_LINKED,
-                         StrategyKind.CONTIGUOUS):
+        if self.kind in _LINKED_KINDS:
             return self.model.node_count
         return int(self.model.info["table_entries"])
 
@@ -520,8 +527,10 @@ def build(ensemble, kind=StrategyKind.GPU_VPREDICATED, batch_size: int | None = 
     ``batch_size`` and the other reference kinds reject one.  Any accepted
     kind returns the GPU evaluator (the reference guarantees bit-identical
     scores across strategies), so ``build(ens, "vpredicated", 16)`` works
-    unchanged.  One difference: trees deeper than ``MAX_DEPTH`` raise
-    ``DepthLimitError`` for the linked kinds too (the GPU walk is predicated)."""
+    unchanged.  As in the reference, the predicated kinds raise
+    ``DepthLimitError`` for trees deeper than ``MAX_DEPTH`` while the linked
+    kinds accept them (packed as child-index records, ``TS_PACK_ANY_DEPTH``;
+    ``leaf_indices`` is then unavailable)."""
     kind = StrategyKind(kind)  # ValueError for unknown kinds, as in the reference
     if kind is StrategyKind.GENERATED:
         raise ValueError(

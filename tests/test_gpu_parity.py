@@ -536,3 +536,37 @@ def test_acceptance_random_probes_deep(depth):
     ev = _ev(flat)
     assert np.array_equal(ev.leaf_indices(X), o.astype(np.int64))
     assert np.array_equal(ev.predict_batch(X), s)
+
+
+def test_depth_boundary_per_strategy():
+    # ref tests/test_evaluators.py:50-62: predicated kinds stop at MAX_DEPTH,
+    # linked kinds walk deeper trees
+    from paper_1212_2287_b200 import (DepthLimitError, Ensemble, Node, StrategyKind, Tree, build,
+                                      reference_predict)
+
+    def chain(depth):
+        node = Node.leaf(1.0)
+        for level in range(depth):
+            node = Node.internal(level % 2, 0.5 / (level + 2), node, Node.leaf(2.0 + level))
+        return Tree(node)
+    build(Ensemble(2, [chain(12)]), StrategyKind.PREDICATED)
+    ens17 = Ensemble(2, [chain(17)])
+    with pytest.raises(DepthLimitError):
+        build(ens17, StrategyKind.PREDICATED)
+    with pytest.raises(DepthLimitError):
+        build(ens17, StrategyKind.VPREDICATED, 8)
+    rng = np.random.default_rng(17)
+    X = rng.random((300, 2), dtype=np.float32) * 0.3
+    for kind in (StrategyKind.HEAP_LINKED, StrategyKind.COMPACT_LINKED, StrategyKind.CONTIGUOUS):
+        ev = build(ens17, kind)
+        x = np.full(2, 0.9, dtype=np.float32)
+        assert ev.predict(x) == reference_predict(ens17, x)
+        got = ev.predict_batch(X)
+        assert got.tolist() == [reference_predict(ens17, X[i]) for i in range(len(X))]
+        with pytest.raises(DepthLimitError):
+            ev.leaf_indices(X)
+    deep31 = Ensemble(2, [chain(31)])
+    assert build(deep31, "heap_linked").predict(np.zeros(2, np.float32)) == \
+        reference_predict(deep31, np.zeros(2, np.float32))
+    with pytest.raises(DepthLimitError):
+        build(Ensemble(2, [chain(32)]), "heap_linked")
