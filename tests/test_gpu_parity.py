@@ -570,3 +570,37 @@ def test_depth_boundary_per_strategy():
         reference_predict(deep31, np.zeros(2, np.float32))
     with pytest.raises(DepthLimitError):
         build(Ensemble(2, [chain(32)]), "heap_linked")
+
+
+def _fuzz_case(rng):
+    """A random ensemble mixing every layout the packer chooses: complete
+    trees of assorted depths (streamed), pruned trees (irregular kernel),
+    single leaves, and occasionally feature counts too wide for a tile."""
+    from paper_1212_2287_b200 import Ensemble
+    f = int(rng.choice([1, 3, 17, 136, 700, 3000]))
+    trees = []
+    for _ in range(int(rng.integers(1, 40))):
+        kind = rng.random()
+        if kind < 0.45:
+            tree = _rand_complete(rng, int(rng.integers(0, 11)), f)
+        elif kind < 0.9:
+            tree = _rand_unbalanced(rng, int(rng.integers(1, 15)), f, prune=float(rng.uniform(0.1, 0.6)))
+        else:
+            tree = _rand_complete(rng, 0, f)
+        w = float(rng.choice([1.0, -1.0, 0.0, rng.uniform(-2, 2)]))
+        trees.append((tree, w))
+    n = int(rng.choice([1, 31, 33, 200, 1500]))
+    X = rng.random((n, f), dtype=np.float32)
+    X[rng.random(X.shape) < 0.2] = 0.0
+    X[rng.random(X.shape) < 0.01] = -0.0
+    return Ensemble(f, trees), X
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_fuzz_mixed_models(seed):
+    rng = np.random.default_rng(1000 + seed)
+    ens, X = _fuzz_case(rng)
+    s, o = oracle.COracle(ens.flat().arrays()).score(X, threads=2, with_ordinals=True)
+    ev = _ev(ens)
+    assert np.array_equal(ev.predict_batch(X), s)
+    assert np.array_equal(ev.leaf_indices(X), o.astype(np.int64))

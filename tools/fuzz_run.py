@@ -1,0 +1,19 @@
+"""Long randomized parity run (400 mixed models) on the GPU against the C oracle.
+
+    python tools/fuzz_run.py        # on a GPU box; the suite runs 40 of these
+"""
+import sys, numpy as np
+sys.path.insert(0, "tests"); sys.path.insert(0, ".")
+import oracle
+from test_gpu_parity import _fuzz_case, _ev
+bad = 0
+for seed in range(5000, 5400):
+    rng = np.random.default_rng(seed)
+    ens, X = _fuzz_case(rng)
+    s, o = oracle.COracle(ens.flat().arrays()).score(X, threads=2, with_ordinals=True)
+    ev = _ev(ens)
+    ok = np.array_equal(ev.predict_batch(X), s) and np.array_equal(ev.leaf_indices(X), o.astype(np.int64))
+    if not ok:
+        bad += 1; print("MISMATCH seed", seed)
+    ev.close()
+print("fuzz done, mismatches:", bad)
