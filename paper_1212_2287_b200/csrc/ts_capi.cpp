@@ -7,6 +7,8 @@
 
 #include <algorithm>
 #include <atomic>
+#include <condition_variable>
+#include <thread>
 #include <string>
 #include <unordered_map>
 
@@ -265,6 +267,86 @@ extern "C" void ts_ipc_close(void *dev_ptr) {
     if (dev_ptr) cudaIpcCloseMemHandle(dev_ptr);
 }
 
+namespace {
+
+bool host_pinned(const void *p) {
+    cudaPointerAttributes attr;
+    if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+        cudaGetLastError();  // clear: an unknown host pointer is just pageable
+        return false;
+    }
+    return attr.type == cudaMemoryTypeHost;
+}
+
+// Host copy of a pageable chunk into pinned staging, split over a small
+// persistent thread pool (one memcpy thread cannot keep up with PCIe).
+class CopyPool {
+  public:
+    static CopyPool &get() {
+        // never destroyed: its workers block on the condition variable for the
+        // life of the process, and destroying a condition variable with
+        // waiters would hang (or crash) at exit
+        static CopyPool *pool = new CopyPool();
+        return *pool;
+    }
+    void copy(void *dst, const void *src, size_t bytes) {
+        const size_t parts = bytes < (8u << 20) ? 1 : workers_.size() + 1;
+        if (parts == 1) {
+            memcpy(dst, src, bytes);
+            return;
+        }
+        std::lock_guard<std::mutex> job(job_mu_);  // one split copy at a time
+        const size_t step = (bytes / parts + 4095) & ~(size_t)4095;
+        {
+            std::lock_guard<std::mutex> l(mu_);
+            dst_ = (char *)dst;
+            src_ = (const char *)src;
+            bytes_ = bytes;
+            step_ = step;
+            pending_ = workers_.size();
+            gen_++;
+        }
+        cv_.notify_all();
+        const size_t off = workers_.size() * step;  // the caller's own share: the last part
+        if (off < bytes) memcpy((char *)dst + off, (const char *)src + off, bytes - off);
+        std::unique_lock<std::mutex> l(mu_);
+        done_.wait(l, [this] { return pending_ == 0; });
+    }
+
+  private:
+    CopyPool() {
+        unsigned hw = std::thread::hardware_concurrency();
+        const unsigned n = std::max(1u, std::min(7u, hw > 1 ? hw / 2 : 1u));
+        for (unsigned i = 0; i < n; i++) workers_.emplace_back([this, i] { run(i); });
+        for (auto &t : workers_) t.detach();  // live for the process
+    }
+    void run(unsigned i) {
+        uint64_t seen = 0;
+        for (;;) {
+            std::unique_lock<std::mutex> l(mu_);
+            cv_.wait(l, [&] { return gen_ != seen; });
+            seen = gen_;
+            char *dst = dst_;
+            const char *src = src_;
+            const size_t bytes = bytes_, step = step_;
+            l.unlock();
+            const size_t off = i * step;
+            if (off < bytes) memcpy(dst + off, src + off, std::min(step, bytes - off));
+            l.lock();
+            if (--pending_ == 0) done_.notify_one();
+        }
+    }
+    std::vector<std::thread> workers_;
+    std::mutex job_mu_, mu_;
+    std::condition_variable cv_, done_;
+    char *dst_ = nullptr;
+    const char *src_ = nullptr;
+    size_t bytes_ = 0, step_ = 0, pending_ = 0;
+    uint64_t gen_ = 0;
+};
+
+}  // namespace
+
 extern "C" int ts_score_host(const ts_model *mc, const float *x, int64_t n, int64_t f,
                              double *out) {
     int rc = check_args(mc, x, n, f, f, out);
@@ -279,6 +361,11 @@ extern "C" int ts_score_host(const ts_model *mc, const float *x, int64_t n, int6
     const int64_t row_bytes = f * (int64_t)sizeof(float);
     int64_t chunk = std::max<int64_t>(4096, (64ll << 20) / row_bytes);
     chunk = std::min(chunk, n);
+    // Pageable caller buffers go through pinned staging: the pool copies
+    // chunk i+1 into one pinned buffer while the DMA engine reads the other
+    // (a cudaMemcpyAsync from pageable memory would stage synchronously at
+    // ~10 GB/s); results land in pinned memory and are copied out on the host.
+    const bool x_pinned = host_pinned(x), out_pinned = host_pinned(out);
     cudaError_t e = cudaSuccess;
     if (!s.copy) {
         if ((e = cudaStreamCreateWithFlags(&s.copy, cudaStreamNonBlocking)) ||
@@ -286,7 +373,8 @@ extern "C" int ts_score_host(const ts_model *mc, const float *x, int64_t n, int6
             return cuda_fail(e, "cudaStreamCreate");
         for (int i = 0; i < 2; i++) {
             if ((e = cudaEventCreateWithFlags(&s.copied[i], cudaEventDisableTiming)) ||
-                (e = cudaEventCreateWithFlags(&s.consumed[i], cudaEventDisableTiming)))
+                (e = cudaEventCreateWithFlags(&s.consumed[i], cudaEventDisableTiming)) ||
+                (e = cudaEventCreateWithFlags(&s.d2h[i], cudaEventDisableTiming)))
                 return cuda_fail(e, "cudaEventCreate");
         }
         if ((e = cudaMalloc(&s.status, sizeof(int32_t)))) return cuda_fail(e, "cudaMalloc");
@@ -306,13 +394,28 @@ extern "C" int ts_score_host(const ts_model *mc, const float *x, int64_t n, int6
             return cuda_fail(e, "cudaMalloc(out)");
         s.out_rows = chunk;
     }
+    if (!x_pinned && s.hx_rows < chunk) {
+        for (int i = 0; i < 2; i++) {
+            cudaFreeHost(s.hx[i]);
+            s.hx[i] = nullptr;
+            if ((e = cudaMallocHost(&s.hx[i], chunk * row_bytes)))
+                return cuda_fail(e, "cudaMallocHost(x staging)");
+        }
+        s.hx_rows = chunk;
+    }
+    if (!out_pinned && s.hout_rows < chunk) {
+        for (int i = 0; i < 2; i++) {
+            cudaFreeHost(s.hout[i]);
+            s.hout[i] = nullptr;
+            if ((e = cudaMallocHost(&s.hout[i], chunk * sizeof(double))))
+                return cuda_fail(e, "cudaMallocHost(out staging)");
+        }
+        s.hout_rows = chunk;
+    }
     if ((e = cudaMemsetAsync(s.status, 0, sizeof(int32_t), s.compute)))
         return cuda_fail(e, "cudaMemsetAsync");
     // The compute stream must not start before the status reset; the copy
     // stream's first wait below orders buffer reuse.
-    // Full chunks, then halving pieces over the last two chunks' worth of
-    // rows, so the part not overlapped with a copy (the last piece's kernel
-    // and D2H) is small.
     // On a mid-pipeline error the copies already queued may still read x or
     // write out: drain both streams before handing the buffers back.
     auto drain = [&s](int code) {
@@ -320,6 +423,19 @@ extern "C" int ts_score_host(const ts_model *mc, const float *x, int64_t n, int6
         cudaStreamSynchronize(s.compute);
         return code;
     };
+    // results staged in s.hout[k] waiting to be copied into the caller's out
+    double *pend_dst[2] = {nullptr, nullptr};
+    int64_t pend_rows[2] = {0, 0};
+    auto flush = [&](int k) -> cudaError_t {
+        if (!pend_dst[k]) return cudaSuccess;
+        cudaError_t fe = cudaEventSynchronize(s.d2h[k]);
+        if (fe == cudaSuccess) memcpy(pend_dst[k], s.hout[k], pend_rows[k] * sizeof(double));
+        pend_dst[k] = nullptr;
+        return fe;
+    };
+    // Full chunks, then halving pieces over the last two chunks' worth of
+    // rows, so the part not overlapped with a copy (the last piece's kernel
+    // and D2H) is small.
     int k = 0;
     int64_t rows = 0;
     for (int64_t r0 = 0; r0 < n; r0 += rows, k ^= 1) {
@@ -327,8 +443,15 @@ extern "C" int ts_score_host(const ts_model *mc, const float *x, int64_t n, int6
         rows = left > 2 * chunk ? chunk
                                 : std::min(left, std::max<int64_t>(std::min<int64_t>(4096, chunk),
                                                                    (left + 1) / 2));
+        const float *src = x + r0 * f;
+        if (!x_pinned) {
+            // staging buffer k is free once its previous H2D completed
+            if ((e = cudaEventSynchronize(s.copied[k]))) return drain(cuda_fail(e, "staging"));
+            CopyPool::get().copy(s.hx[k], src, rows * row_bytes);
+            src = s.hx[k];
+        }
         if ((e = cudaStreamWaitEvent(s.copy, s.consumed[k], 0)) ||
-            (e = cudaMemcpyAsync(s.x[k], x + r0 * f, rows * row_bytes, cudaMemcpyHostToDevice,
+            (e = cudaMemcpyAsync(s.x[k], src, rows * row_bytes, cudaMemcpyHostToDevice,
                                  s.copy)) ||
             (e = cudaEventRecord(s.copied[k], s.copy)) ||
             (e = cudaStreamWaitEvent(s.compute, s.copied[k], 0)))
@@ -336,16 +459,26 @@ extern "C" int ts_score_host(const ts_model *mc, const float *x, int64_t n, int6
         double *dout = s.out + k * chunk;
         rc = score_device(m, s.x[k], rows, f, f, dout, nullptr, 0, s.status, s.compute);
         if (rc) return drain(rc);
-        if ((e = cudaEventRecord(s.consumed[k], s.compute)) ||
-            (e = cudaMemcpyAsync(out + r0, dout, rows * sizeof(double), cudaMemcpyDeviceToHost,
-                                 s.compute)))
-            return drain(cuda_fail(e, "host pipeline (D2H)"));
+        if ((e = cudaEventRecord(s.consumed[k], s.compute)))
+            return drain(cuda_fail(e, "host pipeline"));
+        if (out_pinned) {
+            e = cudaMemcpyAsync(out + r0, dout, rows * sizeof(double), cudaMemcpyDeviceToHost,
+                                s.compute);
+        } else {
+            if ((e = flush(k)) == cudaSuccess &&
+                (e = cudaMemcpyAsync(s.hout[k], dout, rows * sizeof(double),
+                                     cudaMemcpyDeviceToHost, s.compute)) == cudaSuccess)
+                e = cudaEventRecord(s.d2h[k], s.compute);
+            pend_dst[k] = out + r0;
+            pend_rows[k] = rows;
+        }
+        if (e != cudaSuccess) return drain(cuda_fail(e, "host pipeline (D2H)"));
     }
     int32_t flag = 0;
     if ((e = cudaMemcpyAsync(&flag, s.status, sizeof(int32_t), cudaMemcpyDeviceToHost,
                              s.compute)) ||
-        (e = cudaStreamSynchronize(s.compute)))
-        return cuda_fail(e, "host pipeline (sync)");
+        (e = cudaStreamSynchronize(s.compute)) || (e = flush(0)) || (e = flush(1)))
+        return drain(cuda_fail(e, "host pipeline (sync)"));
     if (flag) return fail(TS_ERR_NONFINITE, "dataset contains non-finite values");
     return TS_OK;
 }
@@ -364,9 +497,14 @@ extern "C" void ts_free(ts_model *m) {
         cudaFree(s.x[1]);
         cudaFree(s.out);
         cudaFree(s.status);
+        cudaFreeHost(s.hx[0]);
+        cudaFreeHost(s.hx[1]);
+        cudaFreeHost(s.hout[0]);
+        cudaFreeHost(s.hout[1]);
         for (int i = 0; i < 2; i++) {
             if (s.copied[i]) cudaEventDestroy(s.copied[i]);
             if (s.consumed[i]) cudaEventDestroy(s.consumed[i]);
+            if (s.d2h[i]) cudaEventDestroy(s.d2h[i]);
         }
         if (s.copy) cudaStreamDestroy(s.copy);
         if (s.compute) cudaStreamDestroy(s.compute);

@@ -102,6 +102,11 @@ struct HostScratch {
     int64_t x_rows = 0, out_rows = 0;
     cudaStream_t copy = nullptr, compute = nullptr;
     cudaEvent_t copied[2] = {nullptr, nullptr}, consumed[2] = {nullptr, nullptr};
+    // pinned staging for pageable caller buffers (ts_score_host)
+    float *hx[2] = {nullptr, nullptr};
+    double *hout[2] = {nullptr, nullptr};
+    int64_t hx_rows = 0, hout_rows = 0;
+    cudaEvent_t d2h[2] = {nullptr, nullptr};
 };
 
 }  // namespace ts
