@@ -604,3 +604,24 @@ def test_fuzz_mixed_models(seed):
     ev = _ev(ens)
     assert np.array_equal(ev.predict_batch(X), s)
     assert np.array_equal(ev.leaf_indices(X), o.astype(np.int64))
+
+
+@pytest.mark.parametrize("split", [None, "4"])
+def test_tree_split_across_segments(split, monkeypatch):
+    """Small-batch tree split inside a multi-segment model: each complete
+    segment's fold continues (accumulate) the sum of the segments before it."""
+    from paper_1212_2287_b200 import Ensemble
+    if split:
+        monkeypatch.setenv("TS_SPLIT", split)
+    rng = np.random.default_rng(77)
+    f = 40
+    trees = [(_rand_complete(rng, 8, f), float(rng.uniform(0.5, 1.5))) for _ in range(120)]
+    trees += [(_rand_unbalanced(rng, 9, f), 1.0) for _ in range(15)]
+    trees += [(_rand_complete(rng, 6, f), -0.5) for _ in range(200)]
+    ens = Ensemble(f, trees)
+    X = rng.random((500, f), dtype=np.float32)
+    s, o = oracle.COracle(ens.flat().arrays()).score(X, threads=4, with_ordinals=True)
+    ev = _ev(ens)
+    assert ev.model.info["num_segments"] >= 3
+    assert np.array_equal(ev.predict_batch(X), s)
+    assert np.array_equal(ev.leaf_indices(X), o.astype(np.int64))
