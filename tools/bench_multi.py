@@ -32,6 +32,8 @@ def main():
                                                              "tree-p2p"])
     ap.add_argument("--rows", type=int, default=None)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--check", type=int, default=512,
+                    help="rows checked against the C oracle on the rank holding the result")
     a = ap.parse_args()
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
@@ -61,11 +63,28 @@ def main():
     dist.barrier()
     t = torch.tensor([s.elapsed_time(e) / a.reps], device=dev, dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    # parity on the rank that holds full scores: every rank (instance), rank 0
+    # (tree-reduce), the last rank (tree-pipeline, tree-p2p)
+    holder = {"instance": rank, "tree-reduce": 0}.get(a.mode, world - 1)
+    exact = None
+    if a.check and rank == holder:
+        import numpy as np
+        import oracle
+        k = min(a.check, r1 - r0)
+        rows = np.linspace(0, r1 - r0 - 1, k).astype(np.int64)
+        xs = np.concatenate([w.rows(r0 + int(i), 1) for i in rows])
+        ref = oracle.COracle(w.flat.arrays()).score(np.ascontiguousarray(xs), threads=8)
+        got = out.cpu().numpy()[rows]
+        exact = bool(np.array_equal(got, ref)) if a.mode != "tree-reduce" else \
+            bool(np.allclose(got, ref, rtol=1e-12, atol=1e-12))
+    flags = [None] * world
+    dist.all_gather_object(flags, exact)
     if rank == 0:
         evals = w.n * w.flat.num_trees
         print(json.dumps({"mode": a.mode, "world": world, "workload": w.name,
                           "ms_per_pass": float(t.item()),
-                          "tree_evals_per_s": evals / (float(t.item()) / 1e3)}))
+                          "tree_evals_per_s": evals / (float(t.item()) / 1e3),
+                          "parity": [f for f in flags if f is not None]}))
     dist.destroy_process_group()
 
 
