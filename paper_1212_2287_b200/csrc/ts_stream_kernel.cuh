@@ -56,9 +56,10 @@ constexpr int kMaxStages = 4;
 
 // Chains per thread by depth: deeper trees are bigger, so fewer fit in a
 // ring stage (a K-group must fit one stage).  16 chains for d <= 6 measured
-// +4 % on config 2 d = 3/4/6 over 8 (more independent walks to interleave).
+// +4 % on config 2 d = 3/4/6 over 8 (more independent walks to interleave),
+// 32 for d <= 3 another +4 % at d = 3 (but -2 % at d = 4).
 __host__ __device__ constexpr int chains_for_depth(int d) {
-    return d <= 6 ? 16 : d <= 9 ? 8 : d == 10 ? 4 : d == 11 ? 2 : 1;
+    return d <= 3 ? 32 : d <= 6 ? 16 : d <= 9 ? 8 : d == 10 ? 4 : d == 11 ? 2 : 1;
 }
 
 __device__ __forceinline__ uint32_t su32(const void *p) {
