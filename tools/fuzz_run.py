@@ -7,7 +7,9 @@ sys.path.insert(0, "tests"); sys.path.insert(0, ".")
 import oracle
 from test_gpu_parity import _fuzz_case, _ev
 bad = 0
-for seed in range(5000, 5400):
+import os
+lo = int(os.environ.get("FUZZ_SEED0", "5000"))
+for seed in range(lo, lo + int(os.environ.get("FUZZ_N", "400"))):
     rng = np.random.default_rng(seed)
     ens, X = _fuzz_case(rng)
     s, o = oracle.COracle(ens.flat().arrays()).score(X, threads=2, with_ordinals=True)
