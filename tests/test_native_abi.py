@@ -4,6 +4,10 @@ include/treescore_gpu.h declares (no compute calls here)."""
 import os
 import re
 
+import numpy as np
+import pytest
+
+from conftest import has_cuda
 from paper_1212_2287_b200 import _lib
 from paper_1212_2287_b200._build import build
 
@@ -62,3 +66,37 @@ def test_package_build_is_the_reference_build_function():
     import paper_1212_2287_b200 as pkg
     import paper_1212_2287_b200._build  # noqa: F401
     assert callable(pkg.build) and pkg.build.__module__ == "paper_1212_2287_b200.evaluator"
+
+
+def _compile_example(tmp_path):
+    import shutil
+    import subprocess
+    cc = shutil.which("cc") or shutil.which("gcc")
+    if cc is None:
+        pytest.skip("no C compiler")
+    exe = tmp_path / "score_fvec"
+    libdir = os.path.join(ROOT, "paper_1212_2287_b200")
+    subprocess.run([cc, "-O2", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "examples", "score_fvec.c"), "-L", libdir,
+                    "-l:_ts_gpu.so", f"-Wl,-rpath,{libdir}", "-o", str(exe)], check=True)
+    return exe
+
+
+def test_c_example_compiles_against_the_header(tmp_path):
+    """examples/score_fvec.c uses only include/treescore_gpu.h and the .so."""
+    assert _compile_example(tmp_path).exists()
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not has_cuda(), reason="needs a CUDA device")
+def test_c_example_scores_golden_case(tmp_path):
+    import subprocess
+    from paper_1212_2287_b200 import Dataset, write_fvec
+    from conftest import GOLDEN_DIR
+    exe = _compile_example(tmp_path)
+    g = np.load(os.path.join(GOLDEN_DIR, "mixed.npz"))
+    write_fvec(tmp_path / "x.fvec", Dataset(g["X"]))
+    res = subprocess.run([str(exe), os.path.join(GOLDEN_DIR, "mixed.model.txt"),
+                          str(tmp_path / "x.fvec")], capture_output=True, text=True, check=True)
+    got = np.array([float(v) for v in res.stdout.split()])
+    assert np.array_equal(got, g["scores"])
