@@ -183,11 +183,11 @@ struct StreamArgs {
     int32_t *status;
     PipeArgs pipe;
     // > 1: small-batch tree split -- CTA b walks tile b % tiles over chunk
-    // range b / tiles of `splits`, writing each leaf value to leaf_out
-    // ([row / 32][tree - t0][row % 32], leaf_T trees) instead of summing (out
-    // unused); k_fold (ts_stream.cu) then sums them in tree order.
+    // range b / tiles of `splits`, writing each tree's f64 term w * leaf to
+    // leaf_out ([row / 32][tree - t0][row % 32], leaf_T trees) instead of
+    // summing (out unused); k_fold (ts_stream.cu) then adds them in tree order.
     int splits;
-    float *leaf_out;
+    double *leaf_out;
     long long leaf_T;
 };
 // n: rows of the launch (-1 at pack time: shape-independent checks only).

@@ -111,24 +111,26 @@ namespace {
 // ([row/32][tree][row%32], 128 B per tree) into a double-buffered shared
 // tile with cp.async while warp 0 folds the previous tile, one lane per row,
 // acc = acc + w * leaf in tree order (__dmul_rn / __dadd_rn).
-constexpr int kFoldTrees = 128;  // trees per shared tile (16 KB)
-__device__ __forceinline__ void fold_load(float *dst, const float *src, int trees) {
-    // trees * 32 floats = trees * 8 16-byte pieces over 256 threads
+constexpr int kFoldTrees = 96;  // trees per shared tile (24 KB of f64 terms)
+__device__ __forceinline__ void fold_load(double *dst, const double *src, int trees) {
+    // trees * 32 doubles = trees * 16 16-byte pieces over the block's threads
     const uint32_t d0 = (uint32_t)__cvta_generic_to_shared(dst);
-    for (int i = threadIdx.x; i < trees * 8; i += blockDim.x)
+    for (int i = threadIdx.x; i < trees * 16; i += blockDim.x)
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d0 + 16u * i),
-                     "l"(src + 4 * i)
+                     "l"(src + 2 * i)
                      : "memory");
     asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
-__global__ void __launch_bounds__(256) k_fold(const float *leaf, long long T, int t0,
-                                              const double *weight, int unit_w, int accumulate,
-                                              double *out, long long n) {
-    __shared__ __align__(16) float tile[2][kFoldTrees * 32];
+// One CTA per 32 rows: all 8 warps pull the rows' f64 terms (w * leaf, already
+// rounded by the walk) into double-buffered shared tiles with cp.async; warp 0
+// adds them, one lane per row, in tree order -- a bare DADD chain.
+__global__ void __launch_bounds__(256) k_fold(const double *terms, long long T,
+                                              int accumulate, double *out, long long n) {
+    __shared__ __align__(16) double tile[2][kFoldTrees * 32];
     const long long blk = blockIdx.x;
     const long long row = blk * 32 + (threadIdx.x & 31);
-    const float *src = leaf + blk * T * 32;
+    const double *src = terms + blk * T * 32;
     double acc = 0.0;
     if (threadIdx.x < 32 && accumulate && row < n) acc = out[row];
     const int ntile = (int)((T + kFoldTrees - 1) / kFoldTrees);
@@ -145,13 +147,9 @@ __global__ void __launch_bounds__(256) k_fold(const float *leaf, long long T, in
         }
         __syncthreads();
         if (threadIdx.x < 32) {
-            const float *lv = tile[i & 1] + threadIdx.x;
-            if (unit_w) {
-                for (int t = 0; t < nt; t++) acc = __dadd_rn(acc, (double)lv[t * 32]);
-            } else {
-                for (int t = 0; t < nt; t++)
-                    acc = __dadd_rn(acc, __dmul_rn(__ldg(weight + t0 + tb + t), (double)lv[t * 32]));
-            }
+            const double *lv = tile[i & 1] + threadIdx.x;
+#pragma unroll 8
+            for (int t = 0; t < nt; t++) acc = __dadd_rn(acc, lv[t * 32]);
         }
         __syncthreads();  // tile (i & 1) is refilled next iteration
     }
@@ -162,8 +160,9 @@ __global__ void __launch_bounds__(256) k_fold(const float *leaf, long long T, in
 // Small batches leave most SMs idle (one CTA walks ALL trees of its tile), so
 // when the tiles fill less than half of the resident CTA slots the segment's
 // chunks are split over `splits` CTAs per tile: phase 1 walks and stores each
-// leaf value (stream-ordered scratch from the device's memory pool), phase 2
-// (k_fold) sums them in tree order -- bit-identical to the one-pass kernel.
+// tree's f64 term w * leaf (stream-ordered scratch from the library's memory
+// pool), phase 2 (k_fold) adds them in tree order -- bit-identical to the
+// one-pass kernel.
 // TS_SPLIT=0 disables, TS_SPLIT=J forces J splits (A/B experiments).
 cudaError_t launch_stream(int D, const StreamArgs &a0, int device, cudaStream_t stream) {
     if (a0.n <= 0) return cudaSuccess;
@@ -184,13 +183,13 @@ cudaError_t launch_stream(int D, const StreamArgs &a0, int device, cudaStream_t 
         splits = f <= 0 ? 1 : std::min(f, nchunks);
     }
     const long long blocks = (a.n + 31) / 32;
-    const size_t scratch_bytes = (size_t)blocks * 32 * (size_t)T * sizeof(float);
+    const size_t scratch_bytes = (size_t)blocks * 32 * (size_t)T * sizeof(double);
     if (splits < 2 || a.pipe.flags_in || a.pipe.sums_out || scratch_bytes > (256u << 20))
         return stream_detail::kStreamTable[D](a, device, stream);
 
     cudaMemPool_t pool = scratch_pool(device);
     if (!pool) return stream_detail::kStreamTable[D](a, device, stream);
-    float *scratch = nullptr;
+    double *scratch = nullptr;
     cudaError_t e = cudaMallocFromPoolAsync((void **)&scratch, scratch_bytes, pool, stream);
     if (e != cudaSuccess) return e;
     StreamArgs w = a;
@@ -201,8 +200,7 @@ cudaError_t launch_stream(int D, const StreamArgs &a0, int device, cudaStream_t 
     w.accumulate = 0;
     e = stream_detail::kStreamTable[D](w, device, stream);
     if (e == cudaSuccess) {
-        k_fold<<<(unsigned)blocks, 256, 0, stream>>>(scratch, T, a.t0, a.weight, a.unit_w,
-                                                      a.accumulate, a.out, a.n);
+        k_fold<<<(unsigned)blocks, 256, 0, stream>>>(scratch, T, a.accumulate, a.out, a.n);
         count_launch();
         e = cudaGetLastError();
     }

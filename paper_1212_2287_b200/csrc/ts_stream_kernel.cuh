@@ -305,12 +305,13 @@ __device__ __forceinline__ void walk_group(uint32_t tree0, uint32_t xr, double &
         if constexpr (D > S) h = (u[k] - (base + R::kFid0 - FW * (1u << S))) / FW;
         else h = ((p[k] - base) >> 3) + 1u;
         const float lv = ldsf(base + R::kLeaf0 + 4u * (h - (1u << D)));
-        if constexpr (UNIT_W) acc = __dadd_rn(acc, (double)lv);
-        else acc = __dadd_rn(acc, __dmul_rn(__ldg(a.weight + t + k), (double)lv));
+        // w * leaf rounded to f64 first, then the add (never an FMA)
+        const double term = UNIT_W ? (double)lv : __dmul_rn(__ldg(a.weight + t + k), (double)lv);
+        acc = __dadd_rn(acc, term);
         if constexpr (ORD) {
             if (a.ord && valid) a.ord[(long long)(t + k) * a.ld_ord + row] = (uint16_t)(h - (1u << D));
             if (a.leaf_out)  // tree-split mode: [row / 32][tree][row % 32] for k_fold
-                a.leaf_out[((row >> 5) * a.leaf_T + (t + k - a.t0)) * 32 + (row & 31)] = lv;
+                a.leaf_out[((row >> 5) * a.leaf_T + (t + k - a.t0)) * 32 + (row & 31)] = term;
         }
     }
 }
