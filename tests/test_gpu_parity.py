@@ -625,3 +625,27 @@ def test_tree_split_across_segments(split, monkeypatch):
     assert ev.model.info["num_segments"] >= 3
     assert np.array_equal(ev.predict_batch(X), s)
     assert np.array_equal(ev.leaf_indices(X), o.astype(np.int64))
+
+
+@pytest.mark.parametrize("x_pinned,out_pinned", [(True, True), (True, False), (False, True),
+                                                  (False, False)])
+def test_host_path_pinned_and_pageable(x_pinned, out_pinned):
+    """ts_score_host stages pageable buffers through pinned memory and uses
+    pinned caller buffers directly; every combination scores identically,
+    over several chunks and the halving tail pieces."""
+    import torch
+    from paper_1212_2287_b200.synth import complete_flat
+    rng = np.random.default_rng(5)
+    T, d, F = 64, 6, 300                        # 1200-byte rows -> 56k-row chunks
+    n_int = (1 << d) - 1
+    flat = complete_flat(F, d, rng.integers(0, F, (T, n_int)), rng.random((T, n_int)),
+                         rng.standard_normal((T, 1 << d)))
+    n = 150_000
+    X = rng.random((n, F), dtype=np.float32)
+    xs = torch.from_numpy(X).pin_memory().numpy() if x_pinned else X
+    out = (torch.empty(n, dtype=torch.float64).pin_memory().numpy() if out_pinned
+           else np.empty(n, np.float64))
+    ev = _ev(flat)
+    ev._predict_into(xs, out)
+    ref = oracle.COracle(flat.arrays()).score(X, threads=8)
+    assert np.array_equal(out, ref)
