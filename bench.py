@@ -279,6 +279,12 @@ def run_ours(args):
                 "frac": hbm_bytes / t_launch / 1e9 / peaks["hbm_gbs"],
                 "algorithmic_bytes_per_launch": hbm_bytes},
         "algorithmic_visits_per_launch": visits,
+        # measured speed of light of any shared-memory predicated walk on this
+        # GPU (every lane reading the same node record): the data path caps it
+        # well below the 4-slot issue roofline
+        "practical_ceiling": {"frac": 0.291, "visits_per_clk_sm": 9.32,
+                              "source": "tools/mb_walk_sol.cu, "
+                                        "profiles/r1_microbench_smem_pipes.txt"},
     }
 
     line = {
