@@ -319,7 +319,8 @@ def test_invalid_models_rejected_by_packer():
 
 
 @pytest.mark.parametrize("plan", ["2,8,4,1", "2,8,4,2", "1,8,4,1", "1,8,8,2", "4,8,8,2", "2,16,4,1",
-                                  "1,16,3,1", "1,16,3,2", "8,8,4,1"])
+                                  "1,16,3,1", "1,16,3,2", "8,8,4,1", "4,16,8,1", "2,16,8,1",
+                                  "1,16,8,1", "4,16,4,1"])
 @pytest.mark.parametrize("name", ["wide_irregular", "mixed", "deep_unbalanced"])
 def test_irregular_kernel_shapes(name, plan, monkeypatch):
     """Every k_cstream shape (G instance groups, W walker warps, K chains) the
