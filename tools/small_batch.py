@@ -22,6 +22,8 @@ def main():
     ap.add_argument("--ns", default="1000,10000,100000")
     ap.add_argument("--reps", type=int, default=50)
     ap.add_argument("--graph", action="store_true", help="replay a captured CUDA graph")
+    ap.add_argument("--per-graph", type=int, default=1,
+                    help="launches captured per graph (>1 hides the host's launch cost)")
     a = ap.parse_args()
     rng = np.random.default_rng(5)
     d, T, F = a.depth, a.trees, 136
@@ -39,7 +41,8 @@ def main():
             st = torch.cuda.Stream()
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=st):
-                ev.score_device(x, out)
+                for _ in range(a.per_graph):
+                    ev.score_device(x, out)
             run = g.replay
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
@@ -48,7 +51,7 @@ def main():
             run()
         e.record()
         torch.cuda.synchronize()
-        us = s.elapsed_time(e) * 1e3 / a.reps
+        us = s.elapsed_time(e) * 1e3 / a.reps / (a.per_graph if a.graph else 1)
         got = out.cpu().numpy()
         ref = oracle.COracle(flat.arrays()).score(x.cpu().numpy()[:256], threads=4)
         print(f"d={d} T={T} n={n}: {us:8.1f} us/launch  {n * T / us * 1e6:.3g} evals/s  "
