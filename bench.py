@@ -179,13 +179,20 @@ def run_reference(args):
 def run_ours(args):
     import torch
     ws, rank, local = _dist()
+    # One GPU per rank.  TS_BENCH_BACKEND=gloo (flow tests only: several
+    # independent instance-shard ranks on fewer GPUs, their kernels never wait
+    # on one another) swaps the host-side barrier / max-reduce to gloo; the
+    # numbers of such a run are not scaling numbers.
+    backend = os.environ.get("TS_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
     if ws > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     from paper_1212_2287_b200 import _lib, build_gpu, synth
 
     w = synth.config1(n=N_PER_GPU, shard=rank)
@@ -196,9 +203,18 @@ def run_ours(args):
     stream = torch.cuda.current_stream(dev)
 
     def barrier():
+        torch.cuda.synchronize(dev)
         if ws > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize(dev)
+
+    def max_over_ranks(v: float) -> float:
+        if ws == 1:
+            return v
+        tt = torch.tensor([v], dtype=torch.float64,
+                          device=dev if backend == "nccl" else "cpu")
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        return float(tt.item())
 
     for _ in range(args.warmup):
         ev.score_device(x, out=out)
@@ -217,11 +233,7 @@ def run_ours(args):
     clocks = sampler.stop()
     launches = _lib.launch_count() - launches0
     ms = start.elapsed_time(end)
-    t_max = ms
-    if ws > 1:
-        tt = torch.tensor([ms], dtype=torch.float64, device=dev)
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        t_max = float(tt.item())
+    t_max = max_over_ranks(ms)
     evals = w.n * T * args.steps * ws
     value = evals / (t_max / 1e3)
     ms_per_step = t_max / args.steps
@@ -239,11 +251,7 @@ def run_ours(args):
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
         ev._predict_into(pinned.numpy(), host_out)
-    e2e_s = time.perf_counter() - t0
-    if ws > 1:
-        tt = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
-        e2e_s = float(tt.item())
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
     e2e_value = w.n * T * e2e_steps * ws / e2e_s
     e2e_equal = bool(np.array_equal(host_out, gpu_scores))
 

@@ -35,9 +35,16 @@ def main():
     ap.add_argument("--check", type=int, default=512,
                     help="rows checked against the C oracle on the rank holding the result")
     a = ap.parse_args()
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    # TS_BENCH_BACKEND=gloo: flow test of the instance / tree-reduce modes with
+    # several ranks on fewer GPUs (ranks never wait on one another inside a
+    # kernel); not a scaling measurement.
+    backend = os.environ.get("TS_BENCH_BACKEND", "nccl")
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group(backend)
     world, rank = dist.get_world_size(), dist.get_rank()
     dev = torch.device("cuda", local)
     w = synth.config4a(a.rows or 64_000_000) if a.mode == "instance" \
@@ -61,7 +68,8 @@ def main():
     e.record()
     torch.cuda.synchronize()
     dist.barrier()
-    t = torch.tensor([s.elapsed_time(e) / a.reps], device=dev, dtype=torch.float64)
+    t = torch.tensor([s.elapsed_time(e) / a.reps], dtype=torch.float64,
+                     device=dev if backend == "nccl" else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     # parity on the rank that holds full scores: every rank (instance), rank 0
     # (tree-reduce), the last rank (tree-pipeline, tree-p2p)
