@@ -101,7 +101,11 @@ def main():
                     ev.score_device(x, out=out)
             g.replay()
             torch.cuda.synchronize()
-            reps = max(a.reps, min(400, int(20.0 / max(first_ms * per_graph, 1e-3))))
+            s.record()
+            g.replay()
+            e.record()
+            torch.cuda.synchronize()
+            reps = max(a.reps, min(400, int(20.0 / max(s.elapsed_time(e), 1e-3))))
             s.record()
             for _ in range(reps):
                 g.replay()
