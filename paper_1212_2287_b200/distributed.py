@@ -72,6 +72,28 @@ def tree_shards(depths, world: int) -> list[tuple[int, int]]:
     return [(cuts[i], cuts[i + 1]) for i in range(world)]
 
 
+def table_bytes(flat: FlatModel, depths=None) -> int:
+    """Node-table bytes of the packed ensemble (8-byte nodes and
+    4-byte leaves over each complete tree's heap; irregular trees keep their
+    own nodes as 8-byte child-index records)."""
+    d = np.asarray(flat.depths() if depths is None else depths, dtype=np.int64)
+    nodes = np.diff(np.asarray(flat.tree_off, dtype=np.int64))
+    complete = nodes == (np.int64(2) << d) - 1
+    pw = np.int64(1) << d
+    per_tree = np.where(complete, (pw - 1) * 8 + pw * 4, nodes * 8)
+    return int(per_tree.sum())
+
+
+def choose_mode(flat: FlatModel, l2_bytes: int, depths=None, combine: str = "reduce") -> str:
+    """``"instance"`` while the node tables fit the GPU's L2 (every rank keeps
+    the whole ensemble hot), else tree sharding (north star: the NCCL
+    sum-reduce variant is for tables beyond L2); ``combine`` picks
+    ``"reduce"``, ``"pipeline"`` or ``"p2p"``."""
+    if combine not in ("reduce", "pipeline", "p2p"):
+        raise ValueError(f"unknown combine {combine!r}")
+    return "instance" if table_bytes(flat, depths) <= l2_bytes else f"tree-{combine}"
+
+
 @dataclass
 class ShardPlan:
     mode: str                      # "instance" | "tree-reduce" | "tree-pipeline" | "tree-p2p"
@@ -110,7 +132,8 @@ class ShardedScorer:
     """This rank's share of a sharded scoring job; packs its shard once.
 
     ``x_local``: this rank's instances -- its row shard for ``"instance"``,
-    all ``n_total`` rows for the tree modes.  ``__call__`` returns the rank's
+    all ``n_total`` rows for the tree modes (``self.plan.rows`` either way;
+    ``mode="auto"`` picks between them with :func:`choose_mode`).  ``__call__`` returns the rank's
     row-shard scores for ``"instance"``; for the tree modes the full f64
     ``[n_total]`` scores land on rank 0 (``"tree-reduce"``) or on the last
     rank (``"tree-pipeline"``, ``"tree-p2p"``), partial sums elsewhere.
@@ -118,8 +141,17 @@ class ShardedScorer:
 
     def __init__(self, mode: str, flat: FlatModel, n_total: int, *, group=None,
                  make_scorer: Callable | None = None, device=None, depths=None,
-                 chunk_rows: int = 1 << 17, serialize: bool = False):
+                 chunk_rows: int = 1 << 17, serialize: bool = False,
+                 l2_bytes: int | None = None, combine: str = "reduce"):
         import torch.distributed as dist
+        if mode == "auto":
+            # instance sharding unless the tables exceed L2 (choose_mode); the
+            # caller passes x_local = rows[plan.rows[0]:plan.rows[1]]
+            if l2_bytes is None:
+                import torch
+                dev = torch.cuda.current_device() if device is None else int(device)
+                l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
+            mode = choose_mode(flat, l2_bytes, depths, combine)
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)

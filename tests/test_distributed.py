@@ -40,7 +40,15 @@ def _worker(rank, world, port, mode, q):
     try:
         flat, x = _workload()
         n = x.shape[0]
-        if mode == "instance":
+        if mode.startswith("auto"):
+            # auto:<l2 bytes>: the driver picks the mode from the table size;
+            # the caller scores the rows the plan gives it
+            sc = D.ShardedScorer("auto", flat, n, make_scorer=oracle_scorer, chunk_rows=64,
+                                 l2_bytes=int(mode.split(":")[1]))
+            a, b = sc.plan.rows
+            out = sc(torch.from_numpy(x[a:b]))
+            q.put((rank, (sc.plan.mode, sc.plan.rows), out.numpy().copy(), None))
+        elif mode == "instance":
             a, b = D.row_shard(n, world, rank)
             p, out = D.run_sharded(mode, flat, torch.from_numpy(x[a:b]), n,
                                    make_scorer=oracle_scorer)
@@ -112,3 +120,40 @@ def test_tree_reduce_gloo():
     res = _run("tree-reduce")
     ref = _reference()
     np.testing.assert_allclose(res[0][2], ref, rtol=1e-12, atol=1e-12)
+
+
+def test_table_bytes_and_choose_mode():
+    from paper_1212_2287_b200.synth import complete_flat
+    rng = np.random.default_rng(0)
+    T, d, F = 20, 10, 30
+    n_int = (1 << d) - 1
+    flat = complete_flat(F, d, rng.integers(0, F, (T, n_int)), rng.random((T, n_int)),
+                         rng.standard_normal((T, 1 << d)))
+    per_tree = 8 * n_int + 4 * (1 << d)        # 8-B nodes + 4-B leaves
+    assert D.table_bytes(flat) == T * per_tree
+    # config 4b: 20,000 depth-10 trees = 245.6 MB of tables, beyond a 126 MB L2
+    assert 20_000 * per_tree == 245_600_000
+    irr, _ = _workload()
+    nodes = np.diff(irr.tree_off)
+    assert D.table_bytes(irr) == int((nodes * 8).sum())   # no complete tree among them
+    assert D.choose_mode(flat, T * per_tree) == "instance"
+    assert D.choose_mode(flat, T * per_tree - 1) == "tree-reduce"
+    assert D.choose_mode(flat, 0, combine="pipeline") == "tree-pipeline"
+    with pytest.raises(ValueError):
+        D.choose_mode(flat, 0, combine="bogus")
+
+
+@pytest.mark.parametrize("l2", [1 << 30, 1])
+def test_auto_mode_gloo(l2):
+    """mode="auto": small tables -> instance shards, tables beyond L2 -> tree
+    shards combined by the sum-reduce; both give the reference scores."""
+    res = _run(f"auto:{l2}")
+    ref = _reference()
+    modes = {r[1][0] for r in res}
+    if l2 > 1:
+        assert modes == {"instance"}
+        for rank, (_, (a, b)), out, _ in res:
+            assert np.array_equal(out, ref[a:b])
+    else:
+        assert modes == {"tree-reduce"}
+        np.testing.assert_allclose(res[0][2], ref, rtol=1e-12, atol=1e-12)
