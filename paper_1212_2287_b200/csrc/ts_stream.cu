@@ -33,12 +33,21 @@ extern template cudaError_t launch_d<9>(const StreamArgs &, int, cudaStream_t);
 extern template cudaError_t launch_d<10>(const StreamArgs &, int, cudaStream_t);
 extern template cudaError_t launch_d<11>(const StreamArgs &, int, cudaStream_t);
 extern template cudaError_t launch_d<12>(const StreamArgs &, int, cudaStream_t);
+#define TS_WS_EXTERN(D) extern template cudaError_t launch_ws_d<D>(const StreamArgs &, int, cudaStream_t);
+TS_WS_EXTERN(0) TS_WS_EXTERN(1) TS_WS_EXTERN(2) TS_WS_EXTERN(3) TS_WS_EXTERN(4) TS_WS_EXTERN(5)
+TS_WS_EXTERN(6) TS_WS_EXTERN(7) TS_WS_EXTERN(8) TS_WS_EXTERN(9) TS_WS_EXTERN(10) TS_WS_EXTERN(11)
+TS_WS_EXTERN(12)
+#undef TS_WS_EXTERN
 
 namespace {
 using StreamFn = cudaError_t (*)(const StreamArgs &, int, cudaStream_t);
 const StreamFn kStreamTable[kStreamMaxDepth + 1] = {
     launch_d<0>, launch_d<1>, launch_d<2>, launch_d<3>, launch_d<4>, launch_d<5>,
     launch_d<6>, launch_d<7>, launch_d<8>, launch_d<9>, launch_d<10>, launch_d<11>, launch_d<12>};
+const StreamFn kWsTable[kStreamMaxDepth + 1] = {
+    launch_ws_d<0>, launch_ws_d<1>, launch_ws_d<2>,  launch_ws_d<3>,  launch_ws_d<4>,
+    launch_ws_d<5>, launch_ws_d<6>, launch_ws_d<7>,  launch_ws_d<8>,  launch_ws_d<9>,
+    launch_ws_d<10>, launch_ws_d<11>, launch_ws_d<12>};
 
 }  // namespace
 }  // namespace stream_detail
@@ -103,6 +112,34 @@ bool plan_stream(int F, int D, int device, StreamArgs *a, long long n) {
     }
     if (D <= 9 && plan_stream_cw(F, D, optin, 4, a)) return true;
     return plan_stream_cw(F, D, optin, 8, a);
+}
+
+// Warp-split shape: a 32-row x tile, two fp32 leaf buffers of tpc trees and a
+// ring of 2-4 stages of tpc = kWsWarps * K trees (one K-group per walker warp
+// per chunk), within a third of an SM's shared memory if it fits (three CTAs
+// per SM), else half.
+bool plan_stream_ws(int F, int D, int device, StreamArgs *a) {
+    using namespace stream_detail;
+    if (D > kStreamMaxDepth) return false;
+    const size_t xs = ((size_t)F * 32 * sizeof(float) + 127) & ~(size_t)127;
+    a->fw = split_fid_width(F);
+    a->tree_bytes = split_geom(D, a->fw).bytes;
+    const uint32_t tpc = (uint32_t)(kWsWarps * ws_chains(D));
+    const size_t lb = 2ull * tpc * 32 * sizeof(float);
+    const size_t chunk = ((size_t)tpc * a->tree_bytes + 127) & ~(size_t)127;
+    const size_t bars = (2 * kMaxStages + 4) * 8;
+    for (int ctas = 3; ctas >= 2; ctas--) {
+        const int budget = std::min(dev_attrs(device).smem_optin, 228 * 1024 / ctas - 1024);
+        if (budget <= 0 || xs + lb + bars + 2 * chunk > (size_t)budget) continue;
+        a->cw = ctas;
+        a->xs_bytes = (uint32_t)xs;
+        a->lb_bytes = (uint32_t)lb;
+        a->tpc = (int)tpc;
+        a->chunk_cap = (uint32_t)chunk;
+        a->stages = (int)std::min<size_t>(kMaxStages, ((size_t)budget - xs - lb - bars) / chunk);
+        return true;
+    }
+    return false;
 }
 
 namespace {
@@ -181,6 +218,23 @@ cudaError_t launch_stream(int D, const StreamArgs &a0, int device, cudaStream_t 
     if (const char *e = getenv("TS_SPLIT")) {
         const int f = atoi(e);
         splits = f <= 0 ? 1 : std::min(f, nchunks);
+    }
+    // Warp-split kernel (k_stream_ws) for batches whose 32-row tiles fit one
+    // wave of its CTAs and give every SM one (or whose walk is too short for
+    // the two-pass split): each tile's trees split over four walker warps, no
+    // second pass (r1: cfg0 10.3 -> 8.1 us, 9k rows x 1000 d=8 trees 73 -> 49
+    // us, 1k rows x 100 d=6 trees 10.1 -> 5.1 us; 3k rows x 1000 d=8 trees
+    // stay on the two-pass split, 32 vs 43 us).  Depth <= 8 (deeper trees leave it one
+    // chain per warp).  TS_WS=0|1 disables / forces it (A/B experiments).
+    {
+        StreamArgs w = a;
+        const long long tiles32 = (a.n + 31) / 32;
+        const int sms = dev_attrs(device).sms;
+        const bool fits = D <= 8 && plan_stream_ws(a.F, D, device, &w);
+        bool ws = fits && tiles32 <= (long long)w.cw * sms && (tiles32 >= sms || !long_walk);
+        if (const char *e = getenv("TS_WS")) ws = atoi(e) != 0 && plan_stream_ws(a.F, D, device, &w);
+        if (ws && !a.pipe.flags_in && !a.pipe.sums_out && !getenv("TS_SPLIT"))
+            return stream_detail::kWsTable[D](w, device, stream);
     }
     const long long blocks = (a.n + 31) / 32;
     const size_t scratch_bytes = (size_t)blocks * 32 * (size_t)T * sizeof(double);

@@ -5,6 +5,8 @@
 namespace ts {
 namespace stream_detail {
 template cudaError_t launch_d<6>(const StreamArgs &, int, cudaStream_t);
+template cudaError_t launch_ws_d<6>(const StreamArgs &, int, cudaStream_t);
 template cudaError_t launch_d<7>(const StreamArgs &, int, cudaStream_t);
+template cudaError_t launch_ws_d<7>(const StreamArgs &, int, cudaStream_t);
 }  // namespace stream_detail
 }  // namespace ts

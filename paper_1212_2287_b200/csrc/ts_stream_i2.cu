@@ -5,5 +5,6 @@
 namespace ts {
 namespace stream_detail {
 template cudaError_t launch_d<8>(const StreamArgs &, int, cudaStream_t);
+template cudaError_t launch_ws_d<8>(const StreamArgs &, int, cudaStream_t);
 }  // namespace stream_detail
 }  // namespace ts

@@ -5,7 +5,10 @@
 namespace ts {
 namespace stream_detail {
 template cudaError_t launch_d<10>(const StreamArgs &, int, cudaStream_t);
+template cudaError_t launch_ws_d<10>(const StreamArgs &, int, cudaStream_t);
 template cudaError_t launch_d<11>(const StreamArgs &, int, cudaStream_t);
+template cudaError_t launch_ws_d<11>(const StreamArgs &, int, cudaStream_t);
 template cudaError_t launch_d<12>(const StreamArgs &, int, cudaStream_t);
+template cudaError_t launch_ws_d<12>(const StreamArgs &, int, cudaStream_t);
 }  // namespace stream_detail
 }  // namespace ts

@@ -30,6 +30,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "ts_internal.h"
 
@@ -248,10 +249,14 @@ __device__ __forceinline__ uint32_t sel_ge(float v, float th, uint32_t on_ge, ui
 //    (4/FW) u + per-chain constant, and the step is u -> 2u + (c ? FW - cf : -cf)
 //    with cf = the level-independent fid origin;
 //  * leaf: ordinal from the final state, fp32 leaf value, f64 add in tree order.
-template <int D, int NK, int FW, bool UNIT_W, bool ORD, int CW>
+//  * TERMS (warp-split kernel k_stream_ws): the fp32 leaf value of tree k
+//    goes to the shared leaf buffer at lbt + k * 128 (one 32-row slab per
+//    tree) instead of into acc; the accumulator warp adds w * leaf in tree
+//    order.
+template <int D, int NK, int FW, bool UNIT_W, bool ORD, int CW, bool TERMS = false>
 __device__ __forceinline__ void walk_group(uint32_t tree0, uint32_t xr, double &acc,
                                            const StreamArgs &a, int t, long long row,
-                                           bool valid) {
+                                           bool valid, uint32_t lbt = 0) {
     using R = SplitRec<D, FW>;
     constexpr uint32_t S = R::S;
     constexpr uint32_t TB = R::kBytes;
@@ -306,12 +311,18 @@ __device__ __forceinline__ void walk_group(uint32_t tree0, uint32_t xr, double &
         else h = ((p[k] - base) >> 3) + 1u;
         const float lv = ldsf(base + R::kLeaf0 + 4u * (h - (1u << D)));
         // w * leaf rounded to f64 first, then the add (never an FMA)
-        const double term = UNIT_W ? (double)lv : __dmul_rn(__ldg(a.weight + t + k), (double)lv);
-        acc = __dadd_rn(acc, term);
+        if constexpr (TERMS) {
+            asm volatile("st.shared.f32 [%0], %1;" ::"r"(lbt + k * 128u), "f"(lv) : "memory");
+        } else {
+            const double term =
+                UNIT_W ? (double)lv : __dmul_rn(__ldg(a.weight + t + k), (double)lv);
+            acc = __dadd_rn(acc, term);
+        }
         if constexpr (ORD) {
             if (a.ord && valid) a.ord[(long long)(t + k) * a.ld_ord + row] = (uint16_t)(h - (1u << D));
-            if (a.leaf_out)  // tree-split mode: [row / 32][tree][row % 32] for k_fold
-                a.leaf_out[((row >> 5) * a.leaf_T + (t + k - a.t0)) * 32 + (row & 31)] = term;
+            if (!TERMS && a.leaf_out)  // tree-split mode: [row / 32][tree][row % 32] for k_fold
+                a.leaf_out[((row >> 5) * a.leaf_T + (t + k - a.t0)) * 32 + (row & 31)] =
+                    UNIT_W ? (double)lv : __dmul_rn(__ldg(a.weight + t + k), (double)lv);
         }
     }
 }
@@ -426,6 +437,209 @@ __global__ void __launch_bounds__(Shape<CW>::kThreads, Shape<CW>::kCtasPerSm)
             a.out[row] = acc;
         }
     }
+}
+
+// ---------------------------------------------------------------------------
+// Warp-split variant for small batches (k_stream_ws).  k_stream gives each
+// warp its own 32 rows and ALL trees, so a batch of a few thousand rows
+// occupies a fraction of the SMs and each warp walks the whole ensemble
+// serially.  Here a CTA owns only 32 rows; its kWsWarps walker warps share
+// them and split each chunk's K-groups round-robin; every walk stores its f64
+// term w * leaf in a double-buffered shared leaf buffer lb[tree][row], and an
+// accumulator warp adds the chunk's terms in TREE order (acc = acc + term,
+// __dadd_rn) -- the same sequence of roundings as k_stream, so scores stay
+// bit-identical.  Walkers and accumulator hand buffers over with mbarriers
+// (lbf: written by all walkers, lbe: folded), the producer streams chunks
+// exactly as in k_stream.  Two or three CTAs per SM (plan_stream_ws).
+constexpr int kWsWarps = 4;
+__host__ __device__ constexpr int ws_chains(int d) {
+    return d <= 6 ? 8 : d <= 8 ? 4 : d <= 9 ? 2 : 1;
+}
+
+// Stage 32 rows x F features into xs[f * 32 + r] with all 32 * kWsWarps
+// walker threads (row r = tid % 32, a quarter of the row's columns each).
+__device__ __forceinline__ void stage_rows_ws(const StreamArgs &a, float *xs, long long row0) {
+    constexpr int B = 32;
+    const int tid = threadIdx.x;
+    const int r = tid & 31, q = tid >> 5;
+    const long long row = row0 + r;
+    const bool valid = row < a.n;
+    const float *xrow = a.x + (valid ? row : 0) * a.ld;
+    const int F = a.F;
+    bool bad = false;
+    if (((F & 3) == 0) && ((a.ld & 3) == 0) && ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0)) {
+        const int F4 = F >> 2;
+        const float4 *x4 = reinterpret_cast<const float4 *>(xrow);
+        constexpr int U = 8;
+        for (int c0 = q * U; c0 < F4; c0 += kWsWarps * U) {
+            float4 v[U];
+#pragma unroll
+            for (int u = 0; u < U; u++)
+                v[u] = (valid && c0 + u < F4) ? __ldg(x4 + c0 + u) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                if (c0 + u >= F4) break;
+                bad |= !(finite_f(v[u].x) && finite_f(v[u].y) && finite_f(v[u].z) &&
+                         finite_f(v[u].w));
+                float *dst = xs + 4 * (c0 + u) * B + r;
+                dst[0] = v[u].x;
+                dst[B] = v[u].y;
+                dst[2 * B] = v[u].z;
+                dst[3 * B] = v[u].w;
+            }
+        }
+    } else {
+        for (int c = q; c < F; c += kWsWarps) {
+            const float v = valid ? __ldg(xrow + c) : 0.f;
+            bad |= !finite_f(v);
+            xs[c * B + r] = v;
+        }
+    }
+    if (bad && a.status) atomicOr(a.status, 1);
+}
+
+template <int D, int K, int FW, bool UNIT_W, bool ORD>
+__global__ void __launch_bounds__(32 * (kWsWarps + 2), 3) k_stream_ws(StreamArgs a) {
+    constexpr int B = 32;
+    constexpr int NW = kWsWarps;
+    using R = SplitRec<D, FW>;
+    extern __shared__ __align__(128) unsigned char smem[];
+    float *xs = reinterpret_cast<float *>(smem);
+    unsigned char *lb = smem + a.xs_bytes;  // 2 x tpc x 32 fp32 leaf values
+    unsigned char *ring = lb + a.lb_bytes;
+    const int kStages = a.stages;
+    uint64_t *full = reinterpret_cast<uint64_t *>(ring + kStages * a.chunk_cap);
+    uint64_t *empty = full + kMaxStages;
+    uint64_t *lbf = empty + kMaxStages;  // leaf buffer written (NW walker warps)
+    uint64_t *lbe = lbf + 2;             // leaf buffer folded (accumulator warp)
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kMaxStages; s++) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, NW);
+        }
+        for (int b = 0; b < 2; b++) {
+            mbar_init(lbf + b, NW);
+            mbar_init(lbe + b, 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const long long ntiles = (a.n + B - 1) / B;
+    const int nchunks = (a.t1 - a.t0 + a.tpc - 1) / a.tpc;
+    const uint32_t lb_half = a.lb_bytes / 2;
+
+    if (warp == NW + 1) {  // ---- producer warp: TMA bulk copies (as k_stream)
+        if (lane == 0) {
+            int s = 0;
+            uint32_t ph = 0, used = 0;
+            for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                for (int c = 0; c < nchunks; c++) {
+                    if (used) mbar_wait(empty + s, ph);
+                    const int trees = min(a.tpc, a.t1 - a.t0 - c * a.tpc);
+                    const uint32_t bytes = (uint32_t)trees * a.tree_bytes;
+                    mbar_expect_tx(full + s, bytes);
+                    bulk_g2s(ring + s * a.chunk_cap,
+                             a.blob + a.seg_byte0 + (size_t)c * a.tpc * a.tree_bytes, bytes,
+                             full + s);
+                    if (++s == kStages) {
+                        s = 0;
+                        ph ^= used;
+                        used = 1;
+                    }
+                }
+            }
+        }
+        return;
+    }
+
+    if (warp == NW) {  // ---- accumulator warp: tree-order f64 fold
+        uint32_t it = 0;
+        for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            const long long row = tile * B + lane;
+            const bool valid = row < a.n;
+            double acc = (a.accumulate && valid) ? a.out[row] : 0.0;
+            for (int c = 0; c < nchunks; c++, it++) {
+                const int b = it & 1;
+                const int trees = min(a.tpc, a.t1 - a.t0 - c * a.tpc);
+                mbar_wait(lbf + b, (it >> 1) & 1);
+                const float *lv = reinterpret_cast<const float *>(lb + b * lb_half) + lane;
+                const double *w = a.weight + a.t0 + c * a.tpc;
+                // w * leaf rounded to f64 first (off the DADD chain), then the add
+#pragma unroll 8
+                for (int i = 0; i < trees; i++)
+                    acc = __dadd_rn(acc, UNIT_W ? (double)lv[i * B]
+                                                : __dmul_rn(__ldg(w + i), (double)lv[i * B]));
+                __syncwarp();
+                if (lane == 0) mbar_arrive(lbe + b);
+            }
+            if (valid && a.out) a.out[row] = acc;
+        }
+        return;
+    }
+
+    // ---- walker warps
+    const uint32_t xr = su32(xs) + 4u * lane;
+    int s = 0;
+    uint32_t ph = 0;
+    uint32_t it = 0;
+    double unused = 0.0;
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const long long row = tile * B + lane;
+        const bool valid = row < a.n;
+        consumer_sync<NW * 32>();  // previous tile's walks are done with xs
+        stage_rows_ws(a, xs, tile * B);
+        consumer_sync<NW * 32>();
+        for (int c = 0; c < nchunks; c++, it++) {
+            const int b = it & 1;
+            mbar_wait(full + s, ph);
+            if (it >= 2) mbar_wait(lbe + b, ((it >> 1) - 1) & 1);  // buffer b folded
+            const uint32_t buf = su32(ring + s * a.chunk_cap);
+            const uint32_t lbt = su32(lb + b * lb_half) + 4u * lane;
+            const int t0 = a.t0 + c * a.tpc;
+            const int trees = min(a.tpc, a.t1 - t0);
+            const int ng = trees / K;
+            for (int g = warp; g < ng; g += NW)
+                walk_group<D, K, FW, UNIT_W, ORD, 1, true>(buf + g * K * R::kBytes, xr, unused, a,
+                                                           t0 + g * K, row, valid,
+                                                           lbt + g * K * 128u);
+            for (int k = ng * K + warp; k < trees; k += NW)
+                walk_group<D, 1, FW, UNIT_W, ORD, 1, true>(buf + k * R::kBytes, xr, unused, a,
+                                                           t0 + k, row, valid, lbt + k * 128u);
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(empty + s);  // ring stage read
+                mbar_arrive(lbf + b);    // terms published (release orders the stores)
+            }
+            if (++s == kStages) {
+                s = 0;
+                ph ^= 1u;
+            }
+        }
+    }
+}
+
+template <int D>
+cudaError_t launch_ws_d(const StreamArgs &a, int device, cudaStream_t stream) {
+    constexpr int K = ws_chains(D);
+    auto pick = [&](auto fw) {
+        constexpr int FW = decltype(fw)::value;
+        if (a.ord) return a.unit_w ? k_stream_ws<D, K, FW, true, true> : k_stream_ws<D, K, FW, false, true>;
+        return a.unit_w ? k_stream_ws<D, K, FW, true, false> : k_stream_ws<D, K, FW, false, false>;
+    };
+    auto kern = a.fw == 1 ? pick(std::integral_constant<int, 1>{})
+                          : pick(std::integral_constant<int, 2>{});
+    const size_t smem = (size_t)a.xs_bytes + a.lb_bytes + (size_t)a.stages * a.chunk_cap +
+                        (2 * kMaxStages + 4) * 8;
+    cudaError_t e = ensure_smem((const void *)kern, smem);
+    if (e != cudaSuccess) return e;
+    const long long tiles = (a.n + 31) / 32;
+    const int sms = dev_attrs(device).sms;
+    const int grid = (int)std::min<long long>(tiles, (long long)a.cw * sms);  // cw: CTAs per SM
+    kern<<<grid, 32 * (kWsWarps + 2), smem, stream>>>(a);
+    count_launch();
+    return cudaGetLastError();
 }
 
 template <int D, int FW, int CW>

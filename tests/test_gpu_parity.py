@@ -650,3 +650,46 @@ def test_host_path_pinned_and_pageable(x_pinned, out_pinned):
     ev._predict_into(xs, out)
     ref = oracle.COracle(flat.arrays()).score(X, threads=8)
     assert np.array_equal(out, ref)
+
+
+@pytest.mark.parametrize("ws", ["0", "1"])
+@pytest.mark.parametrize("d,T,n,F", [(6, 100, 1000, 136), (8, 90, 5000, 40), (3, 37, 70, 13),
+                                     (9, 20, 300, 30), (12, 5, 100, 17), (1, 9, 33, 5),
+                                     (8, 40, 20000, 24)])
+def test_warp_split_kernel(ws, d, T, n, F, monkeypatch):
+    """k_stream_ws (32-row tiles, four walker warps splitting each chunk's
+    trees, an accumulator warp folding leaves in tree order) forced on and off
+    over depths 1-12, ragged row counts, F not a multiple of 4, more tiles
+    than CTAs: scores and ordinals identical to the oracle."""
+    from paper_1212_2287_b200.synth import complete_flat
+    monkeypatch.setenv("TS_WS", ws)
+    rng = np.random.default_rng(d * 1000 + n)
+    n_int = (1 << d) - 1
+    flat = complete_flat(F, d, rng.integers(0, F, (T, n_int)), rng.random((T, n_int)),
+                         rng.standard_normal((T, 1 << d)), weights=rng.uniform(-1.5, 1.5, T))
+    x = rng.random((n, F), dtype=np.float32)
+    x[:, : F // 3] = np.round(x[:, : F // 3] * 8) / 8        # exact ties
+    ev = _ev(flat)
+    s, o = oracle.COracle(flat.arrays()).score(x, threads=4, with_ordinals=True)
+    assert np.array_equal(ev.predict_batch(x), s)
+    assert np.array_equal(ev.leaf_indices(x), o.astype(np.int64))
+
+
+def test_warp_split_strided_and_accumulate(monkeypatch):
+    """k_stream_ws on a strided device view (ld > F) inside a multi-segment
+    model (later segments continue the running sums: accumulate)."""
+    import torch
+    from paper_1212_2287_b200 import Ensemble
+    monkeypatch.setenv("TS_WS", "1")
+    rng = np.random.default_rng(5)
+    f = 24
+    trees = [(_rand_complete(rng, 7, f), float(rng.uniform(0.5, 1.5))) for _ in range(50)]
+    trees += [(_rand_unbalanced(rng, 9, f), 1.0) for _ in range(7)]
+    trees += [(_rand_complete(rng, 5, f), -0.25) for _ in range(60)]
+    ens = Ensemble(f, trees)
+    X = rng.random((777, f + 5), dtype=np.float32)
+    s = oracle.COracle(ens.flat().arrays()).score(np.ascontiguousarray(X[:, :f]), threads=4)
+    ev = _ev(ens)
+    assert ev.model.info["num_segments"] >= 3
+    xd = torch.from_numpy(X).cuda()[:, :f]
+    assert np.array_equal(ev.score_device(xd).cpu().numpy(), s)
