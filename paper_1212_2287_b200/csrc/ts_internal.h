@@ -190,11 +190,12 @@ struct StreamArgs {
     double *leaf_out;
     long long leaf_T;
     uint32_t lb_bytes;  // warp-split kernel (k_stream_ws): two tpc x 32 fp32 leaf buffers
+    int ws_ctas;        // warp-split kernel: CTAs per SM (2 or 3)
 };
 // n: rows of the launch (-1 at pack time: shape-independent checks only).
 bool plan_stream(int F, int D, int device, StreamArgs *a, long long n = -1);
 // Warp-split small-batch kernel shape (32-row CTAs, three or two per SM,
-// returned in a->cw); false if it does not fit.
+// returned in a->ws_ctas); false if it does not fit.
 bool plan_stream_ws(int F, int D, int device, StreamArgs *a);
 inline int split_fid_width(int F) { return F <= 256 ? 1 : 2; }
 cudaError_t launch_stream(int D, const StreamArgs &a, int device, cudaStream_t stream);

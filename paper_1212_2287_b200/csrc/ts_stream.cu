@@ -131,7 +131,7 @@ bool plan_stream_ws(int F, int D, int device, StreamArgs *a) {
     for (int ctas = 3; ctas >= 2; ctas--) {
         const int budget = std::min(dev_attrs(device).smem_optin, 228 * 1024 / ctas - 1024);
         if (budget <= 0 || xs + lb + bars + 2 * chunk > (size_t)budget) continue;
-        a->cw = ctas;
+        a->ws_ctas = ctas;
         a->xs_bytes = (uint32_t)xs;
         a->lb_bytes = (uint32_t)lb;
         a->tpc = (int)tpc;
@@ -224,14 +224,15 @@ cudaError_t launch_stream(int D, const StreamArgs &a0, int device, cudaStream_t 
     // the two-pass split): each tile's trees split over four walker warps, no
     // second pass (r1: cfg0 10.3 -> 8.1 us, 9k rows x 1000 d=8 trees 73 -> 49
     // us, 1k rows x 100 d=6 trees 10.1 -> 5.1 us; 3k rows x 1000 d=8 trees
-    // stay on the two-pass split, 32 vs 43 us).  Depth <= 8 (deeper trees leave it one
-    // chain per warp).  TS_WS=0|1 disables / forces it (A/B experiments).
+    // stay on the two-pass split, 32 vs 43 us).  Depth <= 8 (deeper trees
+    // leave it one chain per warp).  TS_WS=0|1 disables / forces it (A/B
+    // experiments).
     {
         StreamArgs w = a;
         const long long tiles32 = (a.n + 31) / 32;
         const int sms = dev_attrs(device).sms;
         const bool fits = D <= 8 && plan_stream_ws(a.F, D, device, &w);
-        bool ws = fits && tiles32 <= (long long)w.cw * sms && (tiles32 >= sms || !long_walk);
+        bool ws = fits && tiles32 <= (long long)w.ws_ctas * sms && (tiles32 >= sms || !long_walk);
         if (const char *e = getenv("TS_WS")) ws = atoi(e) != 0 && plan_stream_ws(a.F, D, device, &w);
         if (ws && !a.pipe.flags_in && !a.pipe.sums_out && !getenv("TS_SPLIT"))
             return stream_detail::kWsTable[D](w, device, stream);

@@ -636,7 +636,7 @@ cudaError_t launch_ws_d(const StreamArgs &a, int device, cudaStream_t stream) {
     if (e != cudaSuccess) return e;
     const long long tiles = (a.n + 31) / 32;
     const int sms = dev_attrs(device).sms;
-    const int grid = (int)std::min<long long>(tiles, (long long)a.cw * sms);  // cw: CTAs per SM
+    const int grid = (int)std::min<long long>(tiles, (long long)a.ws_ctas * sms);
     kern<<<grid, 32 * (kWsWarps + 2), smem, stream>>>(a);
     count_launch();
     return cudaGetLastError();
