@@ -93,7 +93,7 @@ bool plan_stream_cw(int F, int D, int optin, int cw, StreamArgs *a) {
     a->xs_bytes = (uint32_t)xs;
     a->tpc = (int)tpc;
     a->stages = stages;
-    a->chunk_cap = (tpc * tb + 127) & ~127u;
+    a->chunk_cap = (tpc * tb + 15) & ~15u;  // TMA bulk copies need 16-byte granules
     return true;
 }
 }  // namespace

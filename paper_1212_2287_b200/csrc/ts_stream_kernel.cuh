@@ -58,9 +58,12 @@ constexpr int kMaxStages = 4;
 // Chains per thread by depth: deeper trees are bigger, so fewer fit in a
 // ring stage (a K-group must fit one stage).  16 chains for d <= 6 measured
 // +4 % on config 2 d = 3/4/6 over 8 (more independent walks to interleave),
-// 32 for d <= 3 another +4 % at d = 3 (but -2 % at d = 4).
+// 32 for d <= 3 another +4 % at d = 3 (but -2 % at d = 4).  d = 10: 5 chains
+// (two stages of five 9312-byte trees fill the 93120 bytes a 256 x 136 tile
+// leaves exactly) measured -8 % time against 4 at F = 100; 6 gained nothing
+// more.  Wider rows fall back to groups of 4 (walk loop below).
 __host__ __device__ constexpr int chains_for_depth(int d) {
-    return d <= 3 ? 32 : d <= 6 ? 16 : d <= 9 ? 8 : d == 10 ? 4 : d == 11 ? 2 : 1;
+    return d <= 3 ? 32 : d <= 6 ? 16 : d <= 9 ? 8 : d == 10 ? 5 : d == 11 ? 2 : 1;
 }
 
 __device__ __forceinline__ uint32_t su32(const void *p) {
@@ -417,6 +420,11 @@ __global__ void __launch_bounds__(Shape<CW>::kThreads, Shape<CW>::kCtasPerSm)
             for (; k + K <= trees; k += K)
                 walk_group<D, K, FW, UNIT_W, ORD, CW>(buf + k * SplitRec<D, FW>::kBytes, xr, acc,
                                                       a, t0 + k, row, valid);
+            if constexpr (K > 4 && K % 4 != 0) {  // chunks the planner cut below K trees
+                for (; k + 4 <= trees; k += 4)
+                    walk_group<D, 4, FW, UNIT_W, ORD, CW>(buf + k * SplitRec<D, FW>::kBytes, xr,
+                                                          acc, a, t0 + k, row, valid);
+            }
             for (; k < trees; k++)
                 walk_group<D, 1, FW, UNIT_W, ORD, CW>(buf + k * SplitRec<D, FW>::kBytes, xr, acc,
                                                       a, t0 + k, row, valid);
