@@ -61,9 +61,11 @@ constexpr int kMaxStages = 4;
 // 32 for d <= 3 another +4 % at d = 3 (but -2 % at d = 4).  d = 10: 5 chains
 // (two stages of five 9312-byte trees fill the 93120 bytes a 256 x 136 tile
 // leaves exactly) measured -8 % time against 4 at F = 100; 6 gained nothing
-// more.  Wider rows fall back to groups of 4 (walk loop below).
+// more.  d = 8: 9 chains (two stages of nine 2400-byte trees in a 128-row
+// CTA's 46 KB ring) +1.5 % over 8 on config 1.  Wider rows fall back to
+// groups of 4 (walk loop below).
 __host__ __device__ constexpr int chains_for_depth(int d) {
-    return d <= 3 ? 32 : d <= 6 ? 16 : d <= 9 ? 8 : d == 10 ? 5 : d == 11 ? 2 : 1;
+    return d <= 3 ? 32 : d <= 6 ? 16 : d == 8 ? 9 : d <= 9 ? 8 : d == 10 ? 5 : d == 11 ? 2 : 1;
 }
 
 __device__ __forceinline__ uint32_t su32(const void *p) {
