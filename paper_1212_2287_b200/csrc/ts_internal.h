@@ -191,6 +191,7 @@ struct StreamArgs {
     long long leaf_T;
     uint32_t lb_bytes;  // warp-split kernel (k_stream_ws): two tpc x 32 fp32 leaf buffers
     int ws_ctas;        // warp-split kernel: CTAs per SM (2 or 3)
+    int k;              // k_stream lockstep chains per thread (chains_for_depth / _fallback)
 };
 // n: rows of the launch (-1 at pack time: shape-independent checks only).
 bool plan_stream(int F, int D, int device, StreamArgs *a, long long n = -1);

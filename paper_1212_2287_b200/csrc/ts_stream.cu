@@ -71,24 +71,32 @@ bool plan_stream_cw(int F, int D, int optin, int cw, StreamArgs *a) {
     const size_t bars = 2 * kMaxStages * 8;
     if (xs + bars + (size_t)2 * tb > (size_t)optin) return false;
     const size_t ring = (size_t)optin - xs - bars;
-    const uint32_t K = chains_for_depth(D);
-    const size_t group = (size_t)K * tb;
+    // the tuned chain count first; the 256-row shape may fall back to
+    // chains_fallback(D) (a second kernel instantiation) before single trees
+    uint32_t K = 0;
     int stages = 0;
     uint32_t tpc = 0;
-    for (int s = kMaxStages; s >= 2 && !stages; s--) {
-        size_t cap = ring / s;
-        if (cap < group) continue;
-        size_t g = cap / group;
-        const size_t soft = 48 * 1024;   // small chunks keep the ring turning over
-        if (g > 1 && g * group > soft) g = std::max<size_t>(1, soft / group);
-        stages = s;
-        tpc = (uint32_t)(g * K);
+    const uint32_t cands[2] = {(uint32_t)chains_for_depth(D), (uint32_t)chains_fallback(D)};
+    for (int ci = 0; ci < (cw == 8 ? 2 : 1) && !stages; ci++) {
+        const size_t group = (size_t)cands[ci] * tb;
+        for (int s = kMaxStages; s >= 2 && !stages; s--) {
+            size_t cap = ring / s;
+            if (cap < group) continue;
+            size_t g = cap / group;
+            const size_t soft = 48 * 1024;   // small chunks keep the ring turning over
+            if (g > 1 && g * group > soft) g = std::max<size_t>(1, soft / group);
+            stages = s;
+            K = cands[ci];
+            tpc = (uint32_t)(g * K);
+        }
     }
     if (!stages) {
         if (cw != 8) return false;  // the 256-row shape handles it better
         stages = 2;                 // not even two K-groups fit: single trees
+        K = cands[1];
         tpc = (uint32_t)std::max<size_t>(1, (ring / 2) / tb);
     }
+    a->k = (int)K;
     a->cw = cw;
     a->xs_bytes = (uint32_t)xs;
     a->tpc = (int)tpc;

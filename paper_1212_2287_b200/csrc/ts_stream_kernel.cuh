@@ -58,14 +58,25 @@ constexpr int kMaxStages = 4;
 // Chains per thread by depth: deeper trees are bigger, so fewer fit in a
 // ring stage (a K-group must fit one stage).  16 chains for d <= 6 measured
 // +4 % on config 2 d = 3/4/6 over 8 (more independent walks to interleave),
-// 32 for d <= 3 another +4 % at d = 3 (but -2 % at d = 4).  d = 10: 5 chains
+// 32 for d <= 3 another +4 % at d = 3 (but -2 % at d = 4).  r1 session-2
+// sweep (config 2, 1M rows x 1000 trees): d = 5-6 24 chains +2.2 % over 16,
+// d = 7 16 chains +8 % over 8; 48 at d = 3, 24 at d = 4 and 9 at d = 9 were
+// within 1 % or slower, 64 at d = 3 -29 %.  d = 10: 5 chains
 // (two stages of five 9312-byte trees fill the 93120 bytes a 256 x 136 tile
 // leaves exactly) measured -8 % time against 4 at F = 100; 6 gained nothing
 // more.  d = 8: 9 chains (two stages of nine 2400-byte trees in a 128-row
-// CTA's 46 KB ring) +1.5 % over 8 on config 1.  Wider rows fall back to
-// groups of 4 (walk loop below).
+// CTA's 46 KB ring) +1.5 % over 8 on config 1.  Rows too wide for that
+// use chains_fallback(d) (a second instantiation picked by the planner).
 __host__ __device__ constexpr int chains_for_depth(int d) {
-    return d <= 3 ? 32 : d <= 6 ? 16 : d == 8 ? 9 : d <= 9 ? 8 : d == 10 ? 5 : d == 11 ? 2 : 1;
+    return d <= 3 ? 32 : d == 4 ? 16 : d <= 6 ? 24 : d == 7 ? 16 : d == 8 ? 9 : d == 9 ? 8
+         : d == 10 ? 5 : d == 11 ? 2 : 1;
+}
+// The second instantiation per depth, for rows too wide to leave room for two
+// stages of the tuned K-group (the chains the r1 session-1 kernel used; a
+// plan with room for neither walks single trees).
+__host__ __device__ constexpr int chains_fallback(int d) {
+    return d <= 3 ? 8 : d == 4 ? 8 : d <= 6 ? 16 : d == 7 ? 8 : d == 8 ? 8 : d == 9 ? 4
+         : d == 10 ? 4 : d == 11 ? 1 : 1;
 }
 
 __device__ __forceinline__ uint32_t su32(const void *p) {
@@ -422,11 +433,6 @@ __global__ void __launch_bounds__(Shape<CW>::kThreads, Shape<CW>::kCtasPerSm)
             for (; k + K <= trees; k += K)
                 walk_group<D, K, FW, UNIT_W, ORD, CW>(buf + k * SplitRec<D, FW>::kBytes, xr, acc,
                                                       a, t0 + k, row, valid);
-            if constexpr (K > 4 && K % 4 != 0) {  // chunks the planner cut below K trees
-                for (; k + 4 <= trees; k += 4)
-                    walk_group<D, 4, FW, UNIT_W, ORD, CW>(buf + k * SplitRec<D, FW>::kBytes, xr,
-                                                          acc, a, t0 + k, row, valid);
-            }
             for (; k < trees; k++)
                 walk_group<D, 1, FW, UNIT_W, ORD, CW>(buf + k * SplitRec<D, FW>::kBytes, xr, acc,
                                                       a, t0 + k, row, valid);
@@ -652,12 +658,19 @@ cudaError_t launch_ws_d(const StreamArgs &a, int device, cudaStream_t stream) {
     return cudaGetLastError();
 }
 
-template <int D, int FW, int CW>
-auto pick_kernel(const StreamArgs &a) {
-    constexpr int K = chains_for_depth(D);
+template <int D, int K, int FW, int CW>
+auto pick_kernel_k(const StreamArgs &a) {
     if (a.ord || a.leaf_out)
         return a.unit_w ? k_stream<D, K, FW, true, true, CW> : k_stream<D, K, FW, false, true, CW>;
     return a.unit_w ? k_stream<D, K, FW, true, false, CW> : k_stream<D, K, FW, false, false, CW>;
+}
+template <int D, int FW, int CW>
+auto pick_kernel(const StreamArgs &a) {
+    constexpr int K = chains_for_depth(D), K2 = chains_fallback(D);
+    if constexpr (K2 != K) {
+        if (a.k == K2) return pick_kernel_k<D, K2, FW, CW>(a);
+    }
+    return pick_kernel_k<D, K, FW, CW>(a);
 }
 
 template <int D, int CW>
