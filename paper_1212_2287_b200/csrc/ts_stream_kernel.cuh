@@ -336,7 +336,11 @@ __device__ __forceinline__ void walk_group(uint32_t tree0, uint32_t xr, double &
         }
         if constexpr (ORD) {
             if (a.ord && valid) a.ord[(long long)(t + k) * a.ld_ord + row] = (uint16_t)(h - (1u << D));
-            if (!TERMS && a.leaf_out)  // tree-split mode: [row / 32][tree][row % 32] for k_fold
+            // tree-split mode: [row / 32][tree][row % 32] for k_fold.  Only rows
+            // < n: the scratch holds ceil(n / 32) blocks, and a 128-row tile's
+            // rows past them would write into whatever the memory pool handed
+            // out next (another stream's scratch -- a concurrent-callers race).
+            if (!TERMS && a.leaf_out && valid)
                 a.leaf_out[((row >> 5) * a.leaf_T + (t + k - a.t0)) * 32 + (row & 31)] =
                     UNIT_W ? (double)lv : __dmul_rn(__ldg(a.weight + t + k), (double)lv);
         }

@@ -280,7 +280,8 @@ def test_tiny_shapes_and_padded_ordinals():
 
 def test_models_on_concurrent_streams():
     import torch
-    w1 = __import__("paper_1212_2287_b200").synth.config2(6, n=5000, trees=64)
+    from paper_1212_2287_b200 import synth
+    w1 = synth.config2(6, n=5000, trees=64)
     ens, g = load_golden("mixed")
     ev1, ev2 = _ev(w1.flat), _ev(ens)
     x1 = torch.from_numpy(w1.x).cuda()
@@ -693,3 +694,49 @@ def test_warp_split_strided_and_accumulate(monkeypatch):
     assert ev.model.info["num_segments"] >= 3
     xd = torch.from_numpy(X).cuda()[:, :f]
     assert np.array_equal(ev.score_device(xd).cpu().numpy(), s)
+
+
+def test_concurrent_callers_share_one_model():
+    """The reference's evaluators are immutable and reentrant:
+    twelve host threads score through ONE model at once -- host buffers
+    (ts_score_host, its staging under a lock) and device tensors on their own
+    streams, batch sizes that pick the warp-split, the two-pass split and the
+    full kernel -- and every result equals the oracle.  (It caught the
+    two-pass split writing rows past n into the next pool allocation.)"""
+    import threading
+
+    import torch
+    from paper_1212_2287_b200.synth import complete_flat
+    rng = np.random.default_rng(11)
+    T, d, F = 400, 7, 50
+    n_int = (1 << d) - 1
+    flat = complete_flat(F, d, rng.integers(0, F, (T, n_int)), rng.random((T, n_int)),
+                         rng.standard_normal((T, 1 << d)), weights=rng.uniform(0.5, 1.5, T))
+    ev = _ev(flat)
+    ref = oracle.COracle(flat.arrays())
+    sizes = [37, 1000, 3000, 9000, 30000, 200, 5000, 60000, 130, 700, 2100, 4999]
+    xs = [rng.random((n, F), dtype=np.float32) for n in sizes]
+    want = [ref.score(x, threads=2) for x in xs]
+    errors = []
+
+    def worker(i):
+        try:
+            stream = torch.cuda.Stream()
+            for rep in range(5):
+                if (i + rep) % 2:
+                    got = ev.predict_batch(xs[i])
+                else:
+                    with torch.cuda.stream(stream):
+                        xd = torch.from_numpy(xs[i]).cuda()
+                        got = ev.score_device(xd).cpu().numpy()
+                if not np.array_equal(got, want[i]):
+                    errors.append((i, rep))
+        except Exception as e:  # noqa: BLE001
+            errors.append((i, repr(e)))
+
+    threads = [threading.Thread(target=worker, args=(i,)) for i in range(len(sizes))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert errors == []
