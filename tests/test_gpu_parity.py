@@ -740,3 +740,29 @@ def test_concurrent_callers_share_one_model():
     for t in threads:
         t.join()
     assert errors == []
+
+
+@pytest.mark.parametrize("env", [("TS_WS", "1"), ("TS_SPLIT", "3"), ("TS_SPLIT", "0")])
+@pytest.mark.parametrize("n,bad_row", [(100, 0), (100, 99), (3000, 2999), (3000, 1500)])
+def test_nonfinite_flagged_on_every_kernel_path(env, n, bad_row, monkeypatch):
+    """A NaN / inf anywhere in the batch raises ValueError whichever complete-
+    tree kernel stages the rows (warp-split, two-pass split, one-pass), on
+    the host path and on a CUDA tensor; clean rows still score exactly."""
+    import torch
+    from paper_1212_2287_b200.synth import complete_flat
+    monkeypatch.setenv(*env)
+    rng = np.random.default_rng(n + bad_row)
+    T, d, F = 60, 6, 20
+    n_int = (1 << d) - 1
+    flat = complete_flat(F, d, rng.integers(0, F, (T, n_int)), rng.random((T, n_int)),
+                         rng.standard_normal((T, 1 << d)))
+    ev = _ev(flat)
+    x = rng.random((n, F), dtype=np.float32)
+    assert np.array_equal(ev.predict_batch(x), oracle.COracle(flat.arrays()).score(x, threads=4))
+    for bad in (np.nan, np.inf, -np.inf):
+        xb = x.copy()
+        xb[bad_row, (bad_row * 7) % F] = bad
+        with pytest.raises(ValueError, match="non-finite"):
+            ev.predict_batch(xb)
+        with pytest.raises(ValueError, match="non-finite"):
+            ev.predict_batch(torch.from_numpy(xb).cuda())
