@@ -357,9 +357,17 @@ extern "C" int ts_score_host(const ts_model *mc, const float *x, int64_t n, int6
     if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
     std::lock_guard<std::mutex> lock(m->scratch_mu);
     HostScratch &s = m->scratch;
-    // Chunk so that H2D of chunk i+1 overlaps the scoring of chunk i.
+    // Chunk so that H2D of chunk i+1 overlaps the scoring of chunk i (and,
+    // for pageable input, the staging copy of chunk i+1 overlaps the DMA of
+    // chunk i): 64 MB chunks, but at least four of them once the batch is
+    // over 16 MB (a 54 MB batch as one chunk serialised copy, DMA and
+    // kernel); smaller batches go in one piece.
     const int64_t row_bytes = f * (int64_t)sizeof(float);
-    int64_t chunk = std::max<int64_t>(4096, (64ll << 20) / row_bytes);
+    const int64_t total = n * row_bytes;
+    int64_t chunk_bytes = 64ll << 20;
+    if (total > (16ll << 20))
+        chunk_bytes = std::min<int64_t>(chunk_bytes, std::max<int64_t>(8ll << 20, total / 4));
+    int64_t chunk = std::max<int64_t>(4096, chunk_bytes / row_bytes);
     chunk = std::min(chunk, n);
     // Pageable caller buffers go through pinned staging: the pool copies
     // chunk i+1 into one pinned buffer while the DMA engine reads the other
