@@ -81,18 +81,31 @@ inline uint32_t complete_tree_bytes(int d) {
 
 // kSplit tree record: [top records][deep thresholds][leaves][deep fids].
 constexpr int kTopLevels = 5;
+// kSplit record of a depth-d tree: top-level records | deep thresholds |
+// deep fids | (16-byte aligned) leaves.  The node part [0, leaf0) is what the
+// shared-memory walk needs; trees with d >= kGLeafDepth stream only that part
+// through the ring and read their leaf from the record in global memory
+// (L2), which doubles the trees in flight (ts_stream_kernel.cuh; at d = 10 it
+// measured 4 % slower: the extra L1TEX wavefronts of the leaf gather cost more
+// than the chains gained).
+constexpr int kGLeafDepth = 11;
 struct SplitGeom {
-    uint32_t thr0, leaf0, fid0, bytes;
+    uint32_t thr0, fid0, leaf0, bytes;
 };
 inline SplitGeom split_geom(int d, int fw) {
     const uint32_t S = d < kTopLevels ? d : kTopLevels;
     const uint32_t deep = (1u << d) - (1u << S);
     SplitGeom g;
     g.thr0 = ((1u << S) - 1u) * 8u;
-    g.leaf0 = g.thr0 + deep * 4u;
-    g.fid0 = g.leaf0 + (1u << d) * 4u;
-    g.bytes = (g.fid0 + deep * (uint32_t)fw + 15u) & ~15u;
+    g.fid0 = g.thr0 + deep * 4u;
+    g.leaf0 = (g.fid0 + deep * (uint32_t)fw + 15u) & ~15u;
+    g.bytes = (g.leaf0 + (1u << d) * 4u + 15u) & ~15u;
     return g;
+}
+// Bytes of one tree in a ring stage: the node part for global-leaf depths.
+inline uint32_t split_ring_bytes(int d, int fw) {
+    const SplitGeom g = split_geom(d, fw);
+    return d >= kGLeafDepth ? g.leaf0 : g.bytes;
 }
 
 struct HostScratch {
@@ -168,7 +181,8 @@ struct StreamArgs {
     int F;
     const unsigned char *blob;
     unsigned long long seg_byte0;  // blob offset of tree t0
-    uint32_t tree_bytes;           // complete_tree_bytes(D)
+    uint32_t tree_bytes;           // split_geom(D, fw).bytes: record stride in the blob
+    uint32_t ring_tree_bytes;      // bytes per tree in a ring stage (split_ring_bytes)
     int tpc;                       // trees per chunk
     uint32_t chunk_cap;            // bytes per ring stage
     int stages;                    // ring stages (2..4)

@@ -67,7 +67,8 @@ bool plan_stream_cw(int F, int D, int optin, int cw, StreamArgs *a) {
     const size_t xs = ((size_t)F * B * sizeof(float) + 127) & ~(size_t)127;
     a->fw = split_fid_width(F);
     a->tree_bytes = split_geom(D, a->fw).bytes;
-    const uint32_t tb = a->tree_bytes;
+    a->ring_tree_bytes = split_ring_bytes(D, a->fw);
+    const uint32_t tb = a->ring_tree_bytes;
     const size_t bars = 2 * kMaxStages * 8;
     if (xs + bars + (size_t)2 * tb > (size_t)optin) return false;
     const size_t ring = (size_t)optin - xs - bars;
@@ -132,9 +133,10 @@ bool plan_stream_ws(int F, int D, int device, StreamArgs *a) {
     const size_t xs = ((size_t)F * 32 * sizeof(float) + 127) & ~(size_t)127;
     a->fw = split_fid_width(F);
     a->tree_bytes = split_geom(D, a->fw).bytes;
+    a->ring_tree_bytes = split_ring_bytes(D, a->fw);
     const uint32_t tpc = (uint32_t)(kWsWarps * ws_chains(D));
     const size_t lb = 2ull * tpc * 32 * sizeof(float);
-    const size_t chunk = ((size_t)tpc * a->tree_bytes + 127) & ~(size_t)127;
+    const size_t chunk = ((size_t)tpc * a->ring_tree_bytes + 127) & ~(size_t)127;
     const size_t bars = (2 * kMaxStages + 4) * 8;
     for (int ctas = 3; ctas >= 2; ctas--) {
         const int budget = std::min(dev_attrs(device).smem_optin, 228 * 1024 / ctas - 1024);

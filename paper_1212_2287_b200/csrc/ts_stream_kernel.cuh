@@ -24,7 +24,9 @@
 //
 // Chunk = `tpc` consecutive trees of one complete segment (all of depth D,
 // so every tree record has the same size and chunk c starts at
-// c * tpc * tree_bytes).  Record layout: kSplit / split_geom (ts_internal.h).
+// c * tpc * tree_bytes).  Record layout: kSplit / split_geom (ts_internal.h);
+// trees of depth >= kGLeafDepth stream only their node part and read leaves
+// from global memory.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -65,18 +67,21 @@ constexpr int kMaxStages = 4;
 // (two stages of five 9312-byte trees fill the 93120 bytes a 256 x 136 tile
 // leaves exactly) measured -8 % time against 4 at F = 100; 6 gained nothing
 // more.  d = 8: 9 chains (two stages of nine 2400-byte trees in a 128-row
-// CTA's 46 KB ring) +1.5 % over 8 on config 1.  Rows too wide for that
-// use chains_fallback(d) (a second instantiation picked by the planner).
+// CTA's 46 KB ring) +1.5 % over 8 on config 1.  d >= 11 streams only the
+// trees' node parts (leaves read from global memory): 4 chains at d = 11, 2
+// at d = 12 (was 2 and 1 with whole records; d = 12 16.7 -> 11.5 ms, d = 11
+// 8.8 -> 7.1 ms).  Rows too wide for that use chains_fallback(d) (a second
+// instantiation picked by the planner).
 __host__ __device__ constexpr int chains_for_depth(int d) {
     return d <= 3 ? 32 : d == 4 ? 16 : d <= 6 ? 24 : d == 7 ? 16 : d == 8 ? 9 : d == 9 ? 8
-         : d == 10 ? 5 : d == 11 ? 2 : 1;
+         : d == 10 ? 5 : d == 11 ? 4 : 2;
 }
 // The second instantiation per depth, for rows too wide to leave room for two
 // stages of the tuned K-group (the chains the r1 session-1 kernel used; a
 // plan with room for neither walks single trees).
 __host__ __device__ constexpr int chains_fallback(int d) {
     return d <= 3 ? 8 : d == 4 ? 8 : d <= 6 ? 16 : d == 7 ? 8 : d == 8 ? 8 : d == 9 ? 4
-         : d == 10 ? 4 : d == 11 ? 1 : 1;
+         : d == 10 ? 4 : d == 11 ? 2 : 1;
 }
 
 __device__ __forceinline__ uint32_t su32(const void *p) {
@@ -234,16 +239,36 @@ __device__ __forceinline__ uint32_t ldsu(uint32_t addr, int fw) {
     return v;
 }
 
-// Compile-time kSplit record geometry (same formula as split_geom).
+// Compile-time kSplit record geometry (same formulas as split_geom and
+// split_ring_bytes).  kRing: a tree's stride in a ring stage.
 template <int D, int FW>
 struct SplitRec {
     static constexpr uint32_t S = D < kTopLevels ? D : kTopLevels;
     static constexpr uint32_t kThr0 = ((1u << S) - 1u) * 8u;
     static constexpr uint32_t kDeep = (1u << D) - (1u << S);
-    static constexpr uint32_t kLeaf0 = kThr0 + kDeep * 4u;
-    static constexpr uint32_t kFid0 = kLeaf0 + (1u << D) * 4u;
-    static constexpr uint32_t kBytes = (kFid0 + kDeep * FW + 15u) & ~15u;
+    static constexpr uint32_t kFid0 = kThr0 + kDeep * 4u;
+    static constexpr uint32_t kLeaf0 = (kFid0 + kDeep * FW + 15u) & ~15u;
+    static constexpr uint32_t kBytes = (kLeaf0 + (1u << D) * 4u + 15u) & ~15u;
+    static constexpr bool kGLeaf = D >= kGLeafDepth;
+    static constexpr uint32_t kRing = kGLeaf ? kLeaf0 : kBytes;
 };
+
+// Producer: chunk c (`trees` trees from tree a.t0 + c * a.tpc) into a ring
+// stage, completing on `bar`.  Whole records in one bulk copy, or for
+// global-leaf depths each tree's node part (kRing bytes) on its own.
+template <int D, int FW>
+__device__ __forceinline__ void produce_chunk(const StreamArgs &a, unsigned char *stage,
+                                              uint64_t *bar, int c, int trees) {
+    using R = SplitRec<D, FW>;
+    const unsigned char *src = a.blob + a.seg_byte0 + (size_t)c * a.tpc * R::kBytes;
+    mbar_expect_tx(bar, (uint32_t)trees * R::kRing);
+    if constexpr (R::kGLeaf) {
+        for (int i = 0; i < trees; i++)
+            bulk_g2s(stage + (size_t)i * R::kRing, src + (size_t)i * R::kBytes, R::kRing, bar);
+    } else {
+        bulk_g2s(stage, src, (uint32_t)trees * R::kBytes, bar);
+    }
+}
 
 // sel = (v >= th) ? on_ge : on_lt, kept as one FSETP + SEL on registers
 // (ptxas otherwise rematerialises the per-chain constants).
@@ -275,7 +300,7 @@ __device__ __forceinline__ void walk_group(uint32_t tree0, uint32_t xr, double &
                                            bool valid, uint32_t lbt = 0) {
     using R = SplitRec<D, FW>;
     constexpr uint32_t S = R::S;
-    constexpr uint32_t TB = R::kBytes;
+    constexpr uint32_t TB = R::kRing;
     constexpr int kShift = FW == 1 ? 2 : 1;  // theta address = u << kShift + kq
     uint32_t p[NK], lo[NK], hi[NK];
 #pragma unroll
@@ -325,7 +350,14 @@ __device__ __forceinline__ void walk_group(uint32_t tree0, uint32_t xr, double &
         uint32_t h;  // 1-based heap index at level D
         if constexpr (D > S) h = (u[k] - (base + R::kFid0 - FW * (1u << S))) / FW;
         else h = ((p[k] - base) >> 3) + 1u;
-        const float lv = ldsf(base + R::kLeaf0 + 4u * (h - (1u << D)));
+        float lv;
+        if constexpr (R::kGLeaf)  // leaves stay in the blob (L2): node parts only in the ring
+            lv = __ldg(reinterpret_cast<const float *>(a.blob + a.seg_byte0 +
+                                                       (size_t)(t + k - a.t0) * R::kBytes +
+                                                       R::kLeaf0) +
+                       (h - (1u << D)));
+        else
+            lv = ldsf(base + R::kLeaf0 + 4u * (h - (1u << D)));
         // w * leaf rounded to f64 first, then the add (never an FMA)
         if constexpr (TERMS) {
             asm volatile("st.shared.f32 [%0], %1;" ::"r"(lbt + k * 128u), "f"(lv) : "memory");
@@ -392,11 +424,7 @@ __global__ void __launch_bounds__(Shape<CW>::kThreads, Shape<CW>::kCtasPerSm)
                 for (int c = cb; c < ce; c++) {
                     if (used) mbar_wait(empty + s, ph);
                     const int trees = min(a.tpc, a.t1 - a.t0 - c * a.tpc);
-                    const uint32_t bytes = (uint32_t)trees * a.tree_bytes;
-                    mbar_expect_tx(full + s, bytes);
-                    bulk_g2s(ring + s * a.chunk_cap,
-                             a.blob + a.seg_byte0 + (size_t)c * a.tpc * a.tree_bytes, bytes,
-                             full + s);
+                    produce_chunk<D, FW>(a, ring + s * a.chunk_cap, full + s, c, trees);
                     if (++s == kStages) {
                         s = 0;
                         ph ^= used;
@@ -435,10 +463,10 @@ __global__ void __launch_bounds__(Shape<CW>::kThreads, Shape<CW>::kCtasPerSm)
             const int trees = min(a.tpc, a.t1 - t0);
             int k = 0;
             for (; k + K <= trees; k += K)
-                walk_group<D, K, FW, UNIT_W, ORD, CW>(buf + k * SplitRec<D, FW>::kBytes, xr, acc,
+                walk_group<D, K, FW, UNIT_W, ORD, CW>(buf + k * SplitRec<D, FW>::kRing, xr, acc,
                                                       a, t0 + k, row, valid);
             for (; k < trees; k++)
-                walk_group<D, 1, FW, UNIT_W, ORD, CW>(buf + k * SplitRec<D, FW>::kBytes, xr, acc,
+                walk_group<D, 1, FW, UNIT_W, ORD, CW>(buf + k * SplitRec<D, FW>::kRing, xr, acc,
                                                       a, t0 + k, row, valid);
             __syncwarp();
             if (lane == 0) mbar_arrive(empty + s);
@@ -558,11 +586,7 @@ __global__ void __launch_bounds__(32 * (kWsWarps + 2), 3) k_stream_ws(StreamArgs
                 for (int c = 0; c < nchunks; c++) {
                     if (used) mbar_wait(empty + s, ph);
                     const int trees = min(a.tpc, a.t1 - a.t0 - c * a.tpc);
-                    const uint32_t bytes = (uint32_t)trees * a.tree_bytes;
-                    mbar_expect_tx(full + s, bytes);
-                    bulk_g2s(ring + s * a.chunk_cap,
-                             a.blob + a.seg_byte0 + (size_t)c * a.tpc * a.tree_bytes, bytes,
-                             full + s);
+                    produce_chunk<D, FW>(a, ring + s * a.chunk_cap, full + s, c, trees);
                     if (++s == kStages) {
                         s = 0;
                         ph ^= used;
@@ -621,11 +645,11 @@ __global__ void __launch_bounds__(32 * (kWsWarps + 2), 3) k_stream_ws(StreamArgs
             const int trees = min(a.tpc, a.t1 - t0);
             const int ng = trees / K;
             for (int g = warp; g < ng; g += NW)
-                walk_group<D, K, FW, UNIT_W, ORD, 1, true>(buf + g * K * R::kBytes, xr, unused, a,
+                walk_group<D, K, FW, UNIT_W, ORD, 1, true>(buf + g * K * R::kRing, xr, unused, a,
                                                            t0 + g * K, row, valid,
                                                            lbt + g * K * 128u);
             for (int k = ng * K + warp; k < trees; k += NW)
-                walk_group<D, 1, FW, UNIT_W, ORD, 1, true>(buf + k * R::kBytes, xr, unused, a,
+                walk_group<D, 1, FW, UNIT_W, ORD, 1, true>(buf + k * R::kRing, xr, unused, a,
                                                            t0 + k, row, valid, lbt + k * 128u);
             __syncwarp();
             if (lane == 0) {
