@@ -280,6 +280,27 @@ __device__ __forceinline__ uint32_t sel_ge(float v, float th, uint32_t on_ge, ui
     return r;
 }
 
+// Global-leaf depths (kGLeaf): a group's leaf loads go out at the end of its
+// walk and are added to acc only after the NEXT group's walk (still in tree
+// order), so their L2 latency hides behind shared-memory work.
+template <int KP>
+struct LeafPend {
+    float lv[KP];
+    int t = 0, n = 0;  // first tree, count
+};
+template <int D, int FW, bool UNIT_W, int KP>
+__device__ __forceinline__ void flush_leaves(LeafPend<KP> &pend, double &acc, const StreamArgs &a) {
+#pragma unroll
+    for (int j = 0; j < KP; j++) {
+        if (j < pend.n) {
+            const double term = UNIT_W ? (double)pend.lv[j]
+                                       : __dmul_rn(__ldg(a.weight + pend.t + j), (double)pend.lv[j]);
+            acc = __dadd_rn(acc, term);
+        }
+    }
+    pend.n = 0;
+}
+
 // Walk NK consecutive trees of one chunk in lockstep (NK independent chains)
 // over the kSplit record (ts_internal.h), tree k at tree0 + k * kBytes.
 //  * top levels (< kTopLevels): the chain state is the record's shared
@@ -294,10 +315,11 @@ __device__ __forceinline__ uint32_t sel_ge(float v, float th, uint32_t on_ge, ui
 //    goes to the shared leaf buffer at lbt + k * 128 (one 32-row slab per
 //    tree) instead of into acc; the accumulator warp adds w * leaf in tree
 //    order.
-template <int D, int NK, int FW, bool UNIT_W, bool ORD, int CW, bool TERMS = false>
+template <int D, int NK, int FW, bool UNIT_W, bool ORD, int CW, bool TERMS = false, int KP = 1>
 __device__ __forceinline__ void walk_group(uint32_t tree0, uint32_t xr, double &acc,
                                            const StreamArgs &a, int t, long long row,
-                                           bool valid, uint32_t lbt = 0) {
+                                           bool valid, uint32_t lbt = 0,
+                                           LeafPend<KP> *pend = nullptr) {
     using R = SplitRec<D, FW>;
     constexpr uint32_t S = R::S;
     constexpr uint32_t TB = R::kRing;
@@ -344,6 +366,8 @@ __device__ __forceinline__ void walk_group(uint32_t tree0, uint32_t xr, double &
             }
         }
     }
+    constexpr bool kDefer = R::kGLeaf && !TERMS;
+    if constexpr (kDefer) flush_leaves<D, FW, UNIT_W, KP>(*pend, acc, a);  // previous group
 #pragma unroll
     for (int k = 0; k < NK; k++) {
         const uint32_t base = tree0 + k * TB;
@@ -358,6 +382,13 @@ __device__ __forceinline__ void walk_group(uint32_t tree0, uint32_t xr, double &
                        (h - (1u << D)));
         else
             lv = ldsf(base + R::kLeaf0 + 4u * (h - (1u << D)));
+        if constexpr (kDefer) {  // added after the next group's walk
+            pend->lv[k] = lv;
+            if (k == NK - 1) {
+                pend->t = t;
+                pend->n = NK;
+            }
+        } else
         // w * leaf rounded to f64 first, then the add (never an FMA)
         if constexpr (TERMS) {
             asm volatile("st.shared.f32 [%0], %1;" ::"r"(lbt + k * 128u), "f"(lv) : "memory");
@@ -448,6 +479,7 @@ __global__ void __launch_bounds__(Shape<CW>::kThreads, Shape<CW>::kCtasPerSm)
         stage_rows<kB>(a, xs, tile * kB);
         consumer_sync<kB>();
         double acc = (a.accumulate && valid) ? a.out[row] : 0.0;
+        LeafPend<K> pend;  // global-leaf depths: the last group's leaves, added late
         // Cross-GPU running-sum pipeline (ts_score_pipe): this warp's 32-row
         // block continues the sums the previous rank published for it.
         const long long blk = tile * (long long)CW + warp;
@@ -463,11 +495,11 @@ __global__ void __launch_bounds__(Shape<CW>::kThreads, Shape<CW>::kCtasPerSm)
             const int trees = min(a.tpc, a.t1 - t0);
             int k = 0;
             for (; k + K <= trees; k += K)
-                walk_group<D, K, FW, UNIT_W, ORD, CW>(buf + k * SplitRec<D, FW>::kRing, xr, acc,
-                                                      a, t0 + k, row, valid);
+                walk_group<D, K, FW, UNIT_W, ORD, CW, false, K>(
+                    buf + k * SplitRec<D, FW>::kRing, xr, acc, a, t0 + k, row, valid, 0, &pend);
             for (; k < trees; k++)
-                walk_group<D, 1, FW, UNIT_W, ORD, CW>(buf + k * SplitRec<D, FW>::kRing, xr, acc,
-                                                      a, t0 + k, row, valid);
+                walk_group<D, 1, FW, UNIT_W, ORD, CW, false, K>(
+                    buf + k * SplitRec<D, FW>::kRing, xr, acc, a, t0 + k, row, valid, 0, &pend);
             __syncwarp();
             if (lane == 0) mbar_arrive(empty + s);
             if (++s == kStages) {
@@ -475,6 +507,7 @@ __global__ void __launch_bounds__(Shape<CW>::kThreads, Shape<CW>::kCtasPerSm)
                 ph ^= 1u;
             }
         }
+        if constexpr (SplitRec<D, FW>::kGLeaf) flush_leaves<D, FW, UNIT_W, K>(pend, acc, a);
         if (a.pipe.sums_out) {
             // publish to the next rank (peer memory over NVLink), then flag
             if (valid) a.pipe.sums_out[row] = acc;

@@ -766,3 +766,27 @@ def test_nonfinite_flagged_on_every_kernel_path(env, n, bad_row, monkeypatch):
             ev.predict_batch(xb)
         with pytest.raises(ValueError, match="non-finite"):
             ev.predict_batch(torch.from_numpy(xb).cuda())
+
+
+@pytest.mark.parametrize("d,T,n", [(11, 37, 700), (12, 23, 530), (12, 3, 40), (12, 180, 300)])
+def test_global_leaf_depths(d, T, n):
+    """Depths >= 11 stream only node parts and add each group's leaves (read
+    from global memory) after the next group's walk: many chunks, a pending
+    group carried across chunks and tiles, non-unit weights, a following
+    segment continuing the sums -- scores and ordinals identical to the oracle."""
+    from paper_1212_2287_b200 import Ensemble
+    from paper_1212_2287_b200.synth import complete_flat
+    rng = np.random.default_rng(d * 100 + T)
+    F = 33
+    n_int = (1 << d) - 1
+    deep = complete_flat(F, d, rng.integers(0, F, (T, n_int)), rng.random((T, n_int)),
+                         rng.standard_normal((T, 1 << d)), weights=rng.uniform(-2, 2, T))
+    ens = deep.to_ensemble()
+    mixed = Ensemble(F, list(ens.trees) + [(_rand_complete(rng, 6, F), 0.75) for _ in range(9)])
+    x = rng.random((n, F), dtype=np.float32)
+    x[:, :5] = np.round(x[:, :5] * 16) / 16                   # exact ties
+    for model in (deep, mixed.flat()):
+        ev = _ev(model)
+        s, o = oracle.COracle(model.arrays()).score(x, threads=4, with_ordinals=True)
+        assert np.array_equal(ev.predict_batch(x), s)
+        assert np.array_equal(ev.leaf_indices(x), o.astype(np.int64))
