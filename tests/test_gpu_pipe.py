@@ -67,8 +67,11 @@ def test_pipe_sequential_bit_exact(world):
     assert np.array_equal(outs[0], ref)
 
 
-def test_pipe_ragged_rows_and_deep_trees():
-    flat, x = _workload(T=20, d=10, F=40, n=33 * 32 + 7, seed=5)
+@pytest.mark.parametrize("d,T", [(10, 20), (12, 9)])
+def test_pipe_ragged_rows_and_deep_trees(d, T):
+    # d = 12: global-leaf mode -- the deferred leaves of the last K-group must
+    # be in the running sums before they are published to the next rank
+    flat, x = _workload(T=T, d=d, F=40, n=33 * 32 + 7, seed=5)
     outs = _run_sequential(flat, x, 2, epochs=1)
     assert np.array_equal(outs[0], oracle.COracle(flat.arrays()).score(x, threads=4))
 
