@@ -18,12 +18,16 @@ cudaError_t launch_w8(const CStreamArgs &a, int device, cudaStream_t stream);
 cudaError_t launch_w16(const CStreamArgs &a, int device, cudaStream_t stream);
 }  // namespace cstream_detail
 
-// Kernel shape: the most lockstep chains (W walker warps x K trees) whose
-// instance tile, double-buffered leaf buffer and >= 2 ring stages of tpc
-// trees (~1.2 KB per 64-leaf tree) fit the opt-in shared memory, with tpc =
-// S*K trees per chunk (every walker warp on every chunk, S = W/G).  Ties go
-// to more stages (up to 3), then the larger tile (fewer tree-stream passes),
-// then more warps.  Two teams on alternate chunks of S*K/2 trees (smaller
+// Kernel shape: the most lockstep chains that actually walk (G row groups x
+// min(S*K, trees per chunk), S = W/G walker warps per group, chunks of at
+// most 64 trees) whose instance tile, double-buffered leaf buffer and >= 2
+// ring stages of tpc trees (~1.2 KB per 64-leaf tree) fit the opt-in shared
+// memory.  Ties go to the smaller K (less lockstep padding), then more
+// stages (up to 3), then two row groups, then more warps.  r1 session 2
+// (tools/irregular_shapes.py, 500k rows x 2000 trees): the old key (W*K)
+// picked 1x16x8 at F = 256 / 400, whose 128 slots half-idle on 64-tree
+// chunks (6.41 / 6.52 ms); this one picks 2x16x4 (5.44 / 5.60 ms), and
+// 2x16x8 at F = 136 (4.99 vs 5.15 ms); F = 700 (config 3) stays 1x16x3.  Two teams on alternate chunks of S*K/2 trees (smaller
 // stages, more of them in flight) are only a fallback: on config 3 the
 // 16x4 two-team shape ran 58.8 ms against 57.8 ms for 16x3 with one team
 // (per-chunk overhead is paid per half as much work).
@@ -60,8 +64,11 @@ bool plan_cstream(int F, int device, CStreamArgs *a) {
             if (stages < 2) continue;
             const size_t stage = std::min<size_t>((room / stages) & ~(size_t)127,
                                                   (size_t)tpc * 2048 + kHeadBytes);
-            const long key = (2 - teams) * 1000000000L + (long)c.W * c.K * 1000000 +
-                             std::min(stages, 3) * 100000 + B * 100 + c.W * 2;
+            // chains that actually walk: a chunk holds tpc <= 64 trees, so S
+            // warps x K of a row group only all work while S * K <= tpc
+            const long eff = (long)c.G * std::min(S * c.K, teams * tpc);
+            const long key = (2 - teams) * 1000000000L + eff * 1000000 + (16 - c.K) * 10000 +
+                             std::min(stages, 3) * 1000 + (c.G == 2 ? 100 : 0) + c.W;
             if (found && key <= best_key) continue;
             found = true;
             best_key = key;
