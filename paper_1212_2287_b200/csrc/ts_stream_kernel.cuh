@@ -551,7 +551,9 @@ __device__ __forceinline__ void stage_rows_ws(const StreamArgs &a, float *xs, lo
     if (((F & 3) == 0) && ((a.ld & 3) == 0) && ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0)) {
         const int F4 = F >> 2;
         const float4 *x4 = reinterpret_cast<const float4 *>(xrow);
-        constexpr int U = 8;
+        // 12 float4 per thread: a row of up to 192 features lands in one
+        // round trip (the latency a small batch waits on)
+        constexpr int U = 12;
         for (int c0 = q * U; c0 < F4; c0 += kWsWarps * U) {
             float4 v[U];
 #pragma unroll
