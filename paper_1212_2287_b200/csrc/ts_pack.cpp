@@ -149,6 +149,17 @@ void fill_split(const int32_t *fid, const float *val, const int32_t *lc, const i
         recs[j].x = hf[j] << kFidShift;
         memcpy(&recs[j].y, &ht[j], 4);
     }
+    if (split_header(depth, fw)) {
+        // heap levels 0-1 as the 16-byte header (ts_internal.h) in record
+        // slots 0-1, slot 2 unused
+        uint32_t hdr[4];
+        hdr[0] = hf[0] | hf[1] << 8 | hf[2] << 16;
+        memcpy(&hdr[1], &ht[0], 4);
+        memcpy(&hdr[2], &ht[1], 4);
+        memcpy(&hdr[3], &ht[2], 4);
+        memcpy(out, hdr, 16);
+        recs[2] = make_uint2(0u, 0u);
+    }
     for (int l = S; l < depth; l++) {
         for (size_t i = 0; i < ((size_t)1 << l); i++) {
             const size_t heap = ((size_t)1 << l) - 1 + i;

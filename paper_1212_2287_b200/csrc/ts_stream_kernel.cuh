@@ -224,6 +224,14 @@ __device__ __forceinline__ uint2 lds64(uint32_t addr) {
     asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
     return v;
 }
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+    TS_DBG(addr, 16);
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(addr));
+    return v;
+}
 __device__ __forceinline__ float ldsf(uint32_t addr) {
     TS_DBG(addr, 4);
     float v;
@@ -303,6 +311,8 @@ __device__ __forceinline__ void flush_leaves(LeafPend<KP> &pend, double &acc, co
 
 // Walk NK consecutive trees of one chunk in lockstep (NK independent chains)
 // over the kSplit record (ts_internal.h), tree k at tree0 + k * kBytes.
+//  * heap levels 0-1 (split_header depths): the 16-byte tree header, one
+//    broadcast LDS.128 (ts_internal.h);
 //  * top levels (< kTopLevels): the chain state is the record's shared
 //    address p; the heap step j -> 2j + 1 + c (the reference's
 //    i = (i<<1)+1+(x >= theta)) becomes p -> 2p + (c ? 16 - base : 8 - base):
@@ -332,8 +342,27 @@ __device__ __forceinline__ void walk_group(uint32_t tree0, uint32_t xr, double &
         lo[k] = 8u - base;
         hi[k] = 16u - base;
     }
+    uint32_t l0 = 0;
+    if constexpr (split_header(D, FW)) {
+        // heap levels 0-1 from the tree's 16-byte header {fid0 | fid1 << 8 |
+        // fid2 << 16, theta0, theta1, theta2}: one broadcast LDS.128 instead
+        // of a broadcast LDS.64 plus a two-address LDS.64 (2 wavefronts)
+        constexpr uint32_t kXB = Shape<CW>::kB * 4u;  // bytes per feature row of the x tile
 #pragma unroll
-    for (uint32_t l = 0; l < S; l++) {
+        for (int k = 0; k < NK; k++) {
+            const uint4 hd = lds128(p[k]);
+            const float v0 = ldsf((hd.x & 0xffu) * kXB + xr);
+            const bool c0 = v0 >= __uint_as_float(hd.y);
+            const uint32_t f1 = __byte_perm(hd.x, 0u, c0 ? 0x4442u : 0x4441u);
+            const float v1 = ldsf(f1 * kXB + xr);
+            const bool c1 = v1 >= __uint_as_float(c0 ? hd.w : hd.z);
+            // level-2 heap index 3 + 2 c0 + c1 at base + 8 * index
+            p[k] += 24u + (c0 ? 16u : 0u) + (c1 ? 8u : 0u);
+        }
+        l0 = 2;
+    }
+#pragma unroll
+    for (uint32_t l = l0; l < S; l++) {
 #pragma unroll
         for (int k = 0; k < NK; k++) {
             const uint2 q = lds64(p[k]);
