@@ -656,7 +656,8 @@ def test_host_path_pinned_and_pageable(x_pinned, out_pinned):
 @pytest.mark.parametrize("ws", ["0", "1"])
 @pytest.mark.parametrize("d,T,n,F", [(6, 100, 1000, 136), (8, 90, 5000, 40), (3, 37, 70, 13),
                                      (9, 20, 300, 30), (12, 5, 100, 17), (1, 9, 33, 5),
-                                     (8, 40, 20000, 24), (6, 50, 3000, 300)])
+                                     (8, 40, 20000, 24), (6, 50, 3000, 300), (2, 30, 500, 1),
+                                     (2, 7, 3000, 3), (5, 64, 777, 2), (7, 33, 4100, 9)])
 def test_warp_split_kernel(ws, d, T, n, F, monkeypatch):
     """k_stream_ws (32-row tiles, four walker warps splitting each chunk's
     trees, an accumulator warp folding leaves in tree order) forced on and off
