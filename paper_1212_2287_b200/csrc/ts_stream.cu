@@ -229,12 +229,14 @@ cudaError_t launch_stream(int D, const StreamArgs &a0, int device, cudaStream_t 
         const int f = atoi(e);
         splits = f <= 0 ? 1 : std::min(f, nchunks);
     }
-    // Warp-split kernel (k_stream_ws) for batches whose 32-row tiles fit one
-    // wave of its CTAs and give every SM one (or whose walk is too short for
-    // the two-pass split): each tile's trees split over four walker warps, no
-    // second pass (r1: cfg0 10.3 -> 8.1 us, 9k rows x 1000 d=8 trees 73 -> 49
-    // us, 1k rows x 100 d=6 trees 10.1 -> 5.1 us; 3k rows x 1000 d=8 trees
-    // stay on the two-pass split, 32 vs 43 us).  Depth <= 8 (deeper trees
+    // Warp-split kernel (k_stream_ws) for batches whose 32-row tiles fill at
+    // most 1.5 waves of its CTAs and give every SM one (or whose walk is too
+    // short for the two-pass split): each tile's trees split over four walker
+    // warps, no second pass (r1: cfg0 10.3 -> 8.1 us, 9k rows x 1000 d=8
+    // trees 73 -> 49 us, 12k x 1000 d=8 98 -> 88 us, 20k x 100 d=6 14.6 ->
+    // 12.1 us, 1k rows x 100 d=6 trees 10.1 -> 5.1 us; at ~2 waves the
+    // one-pass kernel wins again; 3k rows x 1000 d=8 trees stay on the
+    // two-pass split, 32 vs 43 us).  Depth <= 8 (deeper trees
     // leave it one chain per warp).  TS_WS=0|1 disables / forces it (A/B
     // experiments).
     {
@@ -242,7 +244,7 @@ cudaError_t launch_stream(int D, const StreamArgs &a0, int device, cudaStream_t 
         const long long tiles32 = (a.n + 31) / 32;
         const int sms = dev_attrs(device).sms;
         const bool fits = D <= 8 && plan_stream_ws(a.F, D, device, &w);
-        bool ws = fits && tiles32 <= (long long)w.ws_ctas * sms && (tiles32 >= sms || !long_walk);
+        bool ws = fits && 2 * tiles32 <= 3ll * w.ws_ctas * sms && (tiles32 >= sms || !long_walk);
         if (const char *e = getenv("TS_WS")) ws = atoi(e) != 0 && plan_stream_ws(a.F, D, device, &w);
         if (ws && !a.pipe.flags_in && !a.pipe.sums_out && !getenv("TS_SPLIT"))
             return stream_detail::kWsTable[D](w, device, stream);
