@@ -452,22 +452,33 @@ extern "C" int ts_score_host(const ts_model *mc, const float *x, int64_t n, int6
                                 : std::min(left, std::max<int64_t>(std::min<int64_t>(4096, chunk),
                                                                    (left + 1) / 2));
         const float *src = x + r0 * f;
+        // One piece (a batch up to a chunk: the latency case): copy, score
+        // and read back on the compute stream alone, no cross-stream events.
+        // Every earlier call ended with the compute stream drained, which
+        // orders the copy stream's last use of these buffers too.
+        const bool single = r0 == 0 && rows == n;
         if (!x_pinned) {
             // staging buffer k is free once its previous H2D completed
-            if ((e = cudaEventSynchronize(s.copied[k]))) return drain(cuda_fail(e, "staging"));
+            if (!single && (e = cudaEventSynchronize(s.copied[k])))
+                return drain(cuda_fail(e, "staging"));
             CopyPool::get().copy(s.hx[k], src, rows * row_bytes);
             src = s.hx[k];
         }
-        if ((e = cudaStreamWaitEvent(s.copy, s.consumed[k], 0)) ||
-            (e = cudaMemcpyAsync(s.x[k], src, rows * row_bytes, cudaMemcpyHostToDevice,
-                                 s.copy)) ||
-            (e = cudaEventRecord(s.copied[k], s.copy)) ||
-            (e = cudaStreamWaitEvent(s.compute, s.copied[k], 0)))
+        if (single) {
+            if ((e = cudaMemcpyAsync(s.x[k], src, rows * row_bytes, cudaMemcpyHostToDevice,
+                                     s.compute)))
+                return drain(cuda_fail(e, "host pipeline (H2D)"));
+        } else if ((e = cudaStreamWaitEvent(s.copy, s.consumed[k], 0)) ||
+                   (e = cudaMemcpyAsync(s.x[k], src, rows * row_bytes, cudaMemcpyHostToDevice,
+                                        s.copy)) ||
+                   (e = cudaEventRecord(s.copied[k], s.copy)) ||
+                   (e = cudaStreamWaitEvent(s.compute, s.copied[k], 0))) {
             return drain(cuda_fail(e, "host pipeline (H2D)"));
+        }
         double *dout = s.out + k * chunk;
         rc = score_device(m, s.x[k], rows, f, f, dout, nullptr, 0, s.status, s.compute);
         if (rc) return drain(rc);
-        if ((e = cudaEventRecord(s.consumed[k], s.compute)))
+        if (!single && (e = cudaEventRecord(s.consumed[k], s.compute)))
             return drain(cuda_fail(e, "host pipeline"));
         if (out_pinned) {
             e = cudaMemcpyAsync(out + r0, dout, rows * sizeof(double), cudaMemcpyDeviceToHost,
