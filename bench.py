@@ -304,7 +304,9 @@ def run_ours(args):
                    "instances_per_gpu": w.n, "features": F, "trees": T, "depth": D,
                    "parallelism": f"instance-sharded x{ws}",
                    "l2": "inputs (544 MB/GPU) larger than L2; no flush",
-                   "kernel": f"{info['num_segments']} launch(es)/step"},
+                   "kernel": f"{launches / max(1, args.steps):g} launch(es)/step: k_stream over the "
+                             "full waves of 128-row tiles + k_stream_ws on the last partial wave's rows; "
+                             "roofline.achieved is per step (both kernels)"},
         "roofline": roofline,
         "e2e": {"value": e2e_value, "unit": UNIT,
                 "h2d_bytes_per_step": w.n * F * 4, "d2h_bytes_per_step": w.n * 8,

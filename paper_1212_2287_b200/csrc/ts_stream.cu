@@ -251,8 +251,34 @@ cudaError_t launch_stream(int D, const StreamArgs &a0, int device, cudaStream_t 
     }
     const long long blocks = (a.n + 31) / 32;
     const size_t scratch_bytes = (size_t)blocks * 32 * (size_t)T * sizeof(double);
-    if (splits < 2 || a.pipe.flags_in || a.pipe.sums_out || scratch_bytes > (256u << 20))
+    if (splits < 2 || a.pipe.flags_in || a.pipe.sums_out || scratch_bytes > (256u << 20)) {
+        // Wave tail: when the last wave of tiles would leave more than half
+        // the CTA slots idle, the full waves run here and the remaining rows
+        // go to k_stream_ws, whose 32-row tiles spread them over every SM.
+        // Config 1: the 27th wave of 117 tiles cost a whole wave (2.1 % of
+        // the pass); with the tail on k_stream_ws the pass is 0.6 % faster
+        // (the warp-split kernel's own rate is lower).  d = 7-8 only: at d = 3
+        // it measured 1.4 % slower.  TS_WS=0 disables it.
+        const long long waves = tiles / resident, rem = tiles % resident;
+        const char *wse = getenv("TS_WS");
+        if (D >= 7 && D <= 8 && waves >= 1 && rem > 0 && 2 * rem <= resident && !a.pipe.flags_in &&
+            !a.pipe.sums_out && !(wse && atoi(wse) == 0)) {
+            StreamArgs w = a;
+            if (plan_stream_ws(a.F, D, device, &w)) {
+                const long long n_main = waves * resident * B;
+                StreamArgs m = a;
+                m.n = n_main;
+                cudaError_t e = stream_detail::kStreamTable[D](m, device, stream);
+                if (e != cudaSuccess) return e;
+                w.x = a.x + n_main * a.ld;
+                w.n = a.n - n_main;
+                w.out = a.out ? a.out + n_main : nullptr;
+                w.ord = a.ord ? a.ord + n_main : nullptr;  // row offset; ld_ord unchanged
+                return stream_detail::kWsTable[D](w, device, stream);
+            }
+        }
         return stream_detail::kStreamTable[D](a, device, stream);
+    }
 
     cudaMemPool_t pool = scratch_pool(device);
     if (!pool) return stream_detail::kStreamTable[D](a, device, stream);
