@@ -14,6 +14,7 @@
 //     one is walked;
 //   * each consumer thread walks K trees of the chunk in lockstep (K
 //     independent chains for latency hiding), level by level:
+//         levels 0-1 (split_header depths): one 16-byte header (LDS.128)
 //         top levels (< kTopLevels): rec = {fid << 10, theta} (LDS.64),
 //           v = xs[fid][r] (LDS), heap step j -> 2j + 1 + (v >= theta)
 //         deep levels: theta (LDS.32) and fid (LDS.U8/U16) from per-level
@@ -27,6 +28,10 @@
 // c * tpc * tree_bytes).  Record layout: kSplit / split_geom (ts_internal.h);
 // trees of depth >= kGLeafDepth stream only their node part and read leaves
 // from global memory.
+//
+// k_stream_ws (below): the same walk for small batches -- 32-row CTAs whose
+// four walker warps split each chunk's trees, an accumulator warp folding
+// the leaves in tree order; also runs the last partial wave of a large batch.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
