@@ -105,12 +105,13 @@ inline SplitGeom split_geom(int d, int fw) {
 // Heap levels 0-1 as a 16-byte header {fid0 | fid1 << 8 | fid2 << 16, theta0,
 // theta1, theta2} in record slots 0-1 (one broadcast LDS.128 for both levels;
 // single-byte fids).  Per depth as measured (r1 session 2, 1M rows x 1000
-// trees, F = 136): +2-4 % at d = 2, 3, 5, 6, 7, 9; -0.5 % at d = 4 and 8
-// (the headline), neutral at 10-12.
+// trees, F = 136): +2-4 % at d = 2, 3, 5, 6, 7, 9, +1.9 % at d = 4 together
+// with 24 chains (-0.7 % with 16); -0.5 % at d = 8 (the headline), neutral
+// at 10-12.
 #ifdef __CUDACC__
 __host__ __device__
 #endif
-constexpr bool split_header(int d, int fw) { return fw == 1 && d >= 2 && d != 4 && d != 8; }
+constexpr bool split_header(int d, int fw) { return fw == 1 && d >= 2 && d != 8; }
 // Bytes of one tree in a ring stage: the node part for global-leaf depths.
 inline uint32_t split_ring_bytes(int d, int fw) {
     const SplitGeom g = split_geom(d, fw);

@@ -66,7 +66,8 @@ constexpr int kMaxStages = 4;
 // ring stage (a K-group must fit one stage).  16 chains for d <= 6 measured
 // +4 % on config 2 d = 3/4/6 over 8 (more independent walks to interleave),
 // 32 for d <= 3 another +4 % at d = 3 (but -2 % at d = 4).  r1 session-2
-// sweep (config 2, 1M rows x 1000 trees): d = 5-6 24 chains +2.2 % over 16,
+// sweep (config 2, 1M rows x 1000 trees): d = 5-6 24 chains +2.2 % over 16
+// (d = 4: 24 once the level-0/1 header is on, +1.9 %),
 // d = 7 16 chains +8 % over 8; 48 at d = 3, 24 at d = 4 and 9 at d = 9 were
 // within 1 % or slower, 64 at d = 3 -29 %.  d = 10: 5 chains
 // (two stages of five 9312-byte trees fill the 93120 bytes a 256 x 136 tile
@@ -78,7 +79,7 @@ constexpr int kMaxStages = 4;
 // 8.8 -> 7.1 ms).  Rows too wide for that use chains_fallback(d) (a second
 // instantiation picked by the planner).
 __host__ __device__ constexpr int chains_for_depth(int d) {
-    return d <= 3 ? 32 : d == 4 ? 16 : d <= 6 ? 24 : d == 7 ? 16 : d == 8 ? 9 : d == 9 ? 8
+    return d <= 3 ? 32 : d <= 6 ? 24 : d == 7 ? 16 : d == 8 ? 9 : d == 9 ? 8
          : d == 10 ? 5 : d == 11 ? 4 : 2;
 }
 // The second instantiation per depth, for rows too wide to leave room for two
