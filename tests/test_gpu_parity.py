@@ -791,3 +791,27 @@ def test_global_leaf_depths(d, T, n):
         s, o = oracle.COracle(model.arrays()).score(x, threads=4, with_ordinals=True)
         assert np.array_equal(ev.predict_batch(x), s)
         assert np.array_equal(ev.leaf_indices(x), o.astype(np.int64))
+
+
+@pytest.mark.parametrize("d", [7, 8])
+def test_wave_tail_on_warp_split_kernel(d):
+    """Past one full wave of 128-row tiles, the last partial wave's rows run
+    on k_stream_ws (d = 7-8): scores, ordinals and a following segment's
+    continued sums identical to the oracle across the split row."""
+    import torch
+    from paper_1212_2287_b200 import Ensemble
+    from paper_1212_2287_b200.synth import complete_flat
+    rng = np.random.default_rng(d)
+    T, F = 24, 30
+    n_int = (1 << d) - 1
+    flat = complete_flat(F, d, rng.integers(0, F, (T, n_int)), rng.random((T, n_int)),
+                         rng.standard_normal((T, 1 << d)), weights=rng.uniform(0.5, 1.5, T))
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    n = 2 * sms * 128 + 777                      # one full wave + a short tail
+    x = rng.random((n, F), dtype=np.float32)
+    mixed = Ensemble(F, list(flat.to_ensemble().trees) + [(_rand_complete(rng, 5, F), -0.5)])
+    for model in (flat, mixed.flat()):
+        ev = _ev(model)
+        s, o = oracle.COracle(model.arrays()).score(x, threads=8, with_ordinals=True)
+        assert np.array_equal(ev.predict_batch(x), s)
+        assert np.array_equal(ev.leaf_indices(x), o.astype(np.int64))
