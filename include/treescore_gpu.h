@@ -116,7 +116,11 @@ int ts_model_get_info(const ts_model *model, ts_model_info *info);
  *            (tree-major so that rows are contiguous), ld_ord >= n
  *   status   nullable; int32 device word, OR-ed with 1 if any x is NaN/inf
  *   stream   cudaStream_t (NULL = legacy default stream)
- * Stream-ordered; allocates nothing; returns after enqueueing. */
+ * Stream-ordered; returns after enqueueing.  Allocates nothing from the
+ * caller's heaps: small batches with long walks (the two-pass tree split)
+ * take per-call scratch from the library's own stream-ordered memory pool
+ * (cudaMallocFromPoolAsync / cudaFreeAsync on `stream`, so it stays
+ * CUDA-graph capturable). */
 int ts_score(const ts_model *model, const float *x, int64_t n, int64_t f, int64_t ld,
              double *out, uint16_t *ord_out, int64_t ld_ord, int32_t *status,
              void *stream);
