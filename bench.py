@@ -14,6 +14,21 @@ Under torchrun each rank scores its own 1M-row shard on its own GPU
 (instance sharding, no collective on the data path; "scaling": "weak");
 rank 0 prints one JSON line with the whole-job value (max time over ranks).
 
+Two more measured sub-objects ride on the same line, at the same N:
+``cfg4a`` -- BASELINE config 4a's 64M x 136 matrix split over the N ranks
+(strong scaling; instance sharding, no collective) -- and ``cfg4b`` -- config
+4b's 20,000 depth-10 trees split over the ranks (tree sharding), every rank
+scoring all 8M rows against its shard and ONE NCCL f64 sum-reduce
+(``ts_reduce_partials``, the C ABI's own communicator) combining the partials.
+Each carries ms per pass, tree-evals/s, the efficiency against rank 0 scoring
+the whole job alone in the same run, and an oracle parity sample.
+
+``python bench.py --gpus N`` without a launcher (no WORLD_SIZE in the
+environment) re-executes itself under ``torch.distributed.run`` with N ranks,
+one per GPU (``TS_BENCH_BACKEND=gloo``: host-side plumbing over gloo, ranks
+may share a GPU -- a flow check, not a scaling number).  NCCL_DEBUG=INFO
+stays on for N > 1 so rank counts show in the log.
+
 ``--impl reference`` times the reference algorithm's CPU implementation on
 the host cores (the C restatement in oracle/, all threads, VPred lockstep
 batches) on a bounded row sample of the same workload; rank 0 only.
@@ -106,6 +121,15 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def bench_config(n_gpus: int) -> dict:
+    """The workload's ``config`` -- identical on both arms (same keys, same
+    values) so the driver can match them."""
+    return {"workload": "cfg1: 1M x 136 mixed (ties), T=1000 complete d=8",
+            "instances_per_gpu": N_PER_GPU, "features": F, "trees": T, "depth": D,
+            "parallelism": f"instance-sharded x{n_gpus}",
+            "l2": "inputs (544 MB/GPU) larger than L2; no flush"}
+
+
 def _dist():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -161,12 +185,10 @@ def run_reference(args):
     value = rows * T * args.steps / dt
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
-        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "n_gpus": max(ws, args.gpus), "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32 compare / f64 sum", "data": "synthetic",
-        "config": {"workload": "cfg1: 1M x 136 mixed (ties), T=1000 complete d=8",
-                   "instances": w.n, "features": F, "trees": T, "depth": D,
-                   "sample_rows_per_step": rows},
+        "config": bench_config(max(ws, args.gpus)),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": f"{rows} rows x {T} trees per step (C restatement of the "
                                    "reference VPred path, oracle/ts_oracle.c, v=64)"},
@@ -176,9 +198,189 @@ def run_reference(args):
     return 0
 
 
+class _Ctx:
+    def __init__(self, ws, rank, local, dev, backend, barrier, max_over_ranks):
+        self.ws, self.rank, self.local, self.dev, self.backend = ws, rank, local, dev, backend
+        self.barrier, self.max = barrier, max_over_ranks
+
+    def min(self, v: float) -> float:
+        return -self.max(-float(v))
+
+    def sum(self, v: float) -> float:
+        if self.ws == 1:
+            return float(v)
+        import torch
+        t = torch.tensor([float(v)], dtype=torch.float64,
+                         device=self.dev if self.backend == "nccl" else "cpu")
+        torch.distributed.all_reduce(t)
+        return float(t.item())
+
+
+def _gen_rows(w, row0: int, n: int, dev):
+    """Rows [row0, row0+n) of a counter-based workload, generated on the GPU."""
+    import torch
+    from paper_1212_2287_b200 import _lib
+    x = torch.empty((n, w.f), dtype=torch.float32, device=dev)
+    rc = _lib.load().ts_synth_uniform(x.data_ptr(), n, w.f, w.f, w.hash_seed, row0, w.zero_prob,
+                                      torch.cuda.current_stream(dev).cuda_stream)
+    if rc != 0:
+        raise RuntimeError(f"ts_synth_uniform: {_lib.last_error()}")
+    return x
+
+
+def _time_steps(fn, steps: int, warmup: int, c, dev, sync=None) -> float:
+    """Max over ranks of the mean ms per call of ``fn`` (CUDA events on the
+    current stream, barrier + synchronize on both sides)."""
+    import torch
+    for _ in range(warmup):
+        fn()
+    c.barrier()
+    st = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(steps):
+        fn()
+    e1.record(st)
+    if sync is not None:
+        sync()
+    c.barrier()
+    return c.max(e0.elapsed_time(e1) / steps)
+
+
+def _time_local(fn, steps: int, warmup: int, dev) -> float:
+    """Mean ms per call of ``fn`` on this rank alone (no collectives)."""
+    import torch
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize(dev)
+    st = torch.cuda.current_stream(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(steps):
+        fn()
+    e1.record(st)
+    torch.cuda.synchronize(dev)
+    return e0.elapsed_time(e1) / steps
+
+
+def _roof(n, T, F_, sum_depth, n_gpus, tree_sharded=False):
+    """SURVEY 8(d) roofline in tree-evals/s for N GPUs (tree sharding: every
+    GPU reads all n rows, so the HBM term does not shrink with N)."""
+    import torch
+    peaks = _peaks()
+    n_sm = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    visit_peak = n_sm * 128 * peaks["sm_max_mhz"] * 1e6 / 4
+    t_issue = n * sum_depth / visit_peak / n_gpus
+    t_hbm = n * (4 * F_ + 8) / (peaks["hbm_gbs"] * 1e9) / (1 if tree_sharded else n_gpus)
+    return n * T / max(t_issue, t_hbm)
+
+
+def sub_cfg4a(args, c):
+    """BASELINE config 4a: 64M x 136 U[0,1) rows (34.8 GB) and config 2's
+    depth-8 ensemble, instance-sharded over the N ranks (contiguous row
+    ranges, no collective).  Rank 0 also scores the whole matrix alone: the
+    single-GPU time the efficiency is measured against."""
+    import torch
+    import oracle
+    from paper_1212_2287_b200 import GpuModel, synth
+    from paper_1212_2287_b200.distributed import row_shard
+    w = synth.config4a()
+    n, T_ = w.n, w.flat.num_trees
+    a, b = row_shard(n, c.ws, c.rank)
+    r0, nr = (0, n) if c.rank == 0 else (a, b - a)   # rank 0's shard is a view of all rows
+    x = _gen_rows(w, r0, nr, c.dev)
+    m = GpuModel(w.flat, c.local)
+    out = torch.empty(nr, dtype=torch.float64, device=c.dev)
+    xs, outs = x[a - r0:b - r0], out[a - r0:b - r0]
+    steps, warm = args.sub_steps, 1
+    t_n = _time_steps(lambda: m.score(xs, out=outs), steps, warm, c, c.dev)
+    if c.ws > 1:
+        t1 = _time_local(lambda: m.score(x, out=out), steps, warm, c.dev) \
+            if c.rank == 0 else 0.0
+        t1 = c.max(t1)          # the other ranks wait here
+    else:
+        t1 = t_n
+    rows = oracle.sample_rows(b - a, max(64, 4096 // c.ws), seed=c.rank) + a
+    got = outs.index_select(0, torch.from_numpy(rows - a).to(c.dev)).cpu().numpy()
+    host = np.concatenate([w.rows(s0, k) for s0, k in oracle.runs_of(rows)])
+    ok = bool(np.array_equal(got, oracle.COracle(w.flat.arrays()).score(host)))
+    sd = int(m.info["sum_depth"])
+    res = {"workload": "cfg4a: 64M x 136 U[0,1), T=1000 complete d=8, instance-sharded",
+           "n_gpus": c.ws, "scaling": "strong", "instances": n, "trees": T_,
+           "ms_per_pass": t_n, "tree_evals_per_s": n * T_ / (t_n / 1e3),
+           "single_gpu_ms_per_pass": t1, "efficiency_vs_1gpu": t1 / (c.ws * t_n),
+           "roofline_frac": (n * T_ / (t_n / 1e3)) / _roof(n, T_, w.f, sd, c.ws),
+           "steps": steps, "collective": "none",
+           "parity": {"rows_checked": int(c.sum(len(rows))), "bit_exact_vs_oracle":
+                      bool(c.min(1.0 if ok else 0.0) > 0)}}
+    del x, out, xs, outs
+    m.close()
+    return res
+
+
+def sub_cfg4b(args, c):
+    """BASELINE config 4b: 20,000 depth-10 trees (245.6 MB of node tables,
+    beyond L2) over 8M x 136 rows, tree-sharded: every rank scores all rows
+    against its contiguous tree range (balanced by sum of depths) and one
+    NCCL f64 sum-reduce to rank 0 (``ts_reduce_partials`` through the
+    library's own communicator, async errors polled) combines them.  Rank 0
+    also scores the whole ensemble alone (the single-GPU reference)."""
+    import torch
+    import oracle
+    from paper_1212_2287_b200 import GpuModel, synth
+    w = synth.config4b()
+    n, T_ = w.n, w.flat.num_trees
+    x = _gen_rows(w, 0, n, c.dev)
+    out = torch.zeros(n, dtype=torch.float64, device=c.dev)
+    steps, warm = args.sub_steps, 1
+    full = GpuModel(w.flat, c.local) if c.rank == 0 else None
+    if c.ws > 1:
+        from paper_1212_2287_b200.distributed import ShardedScorer
+        sc = ShardedScorer("tree-reduce", w.flat, n, device=c.local)
+        how = ("ts_reduce_partials (NCCL f64 sum, library communicator)"
+               if sc.reducer is not None else "torch.distributed reduce over gloo (host-staged)")
+        t_n = _time_steps(lambda: sc(x, out), steps, warm, c, c.dev)
+        trees = sc.plan.trees
+        t1 = _time_local(lambda: full.score(x), steps, warm, c.dev) if c.rank == 0 else 0.0
+        t1 = c.max(t1)          # the other ranks wait here
+    else:
+        sc, how, trees = None, "none (one GPU)", (0, T_)
+        t_n = t1 = _time_steps(lambda: full.score(x, out=out), steps, warm, c, c.dev)
+    res = None
+    if c.rank == 0:
+        rows = oracle.sample_rows(n, 1024, seed=41)
+        got = out.index_select(0, torch.from_numpy(rows).to(c.dev)).cpu().numpy()
+        host = np.concatenate([w.rows(s0, k) for s0, k in oracle.runs_of(rows)])
+        orc = oracle.COracle(w.flat.arrays())
+        ref = orc.score(host)
+        tol = oracle.score_tolerance(orc, host, ref)
+        sd = int(full.info["sum_depth"])
+        res = {"workload": "cfg4b: 8M x 136 U[0,1), T=20000 complete d=10, tree-sharded",
+               "n_gpus": c.ws, "scaling": "strong", "instances": n, "trees": T_,
+               "rank0_trees": list(trees), "combine": how,
+               "ms_per_pass": t_n, "tree_evals_per_s": n * T_ / (t_n / 1e3),
+               "single_gpu_ms_per_pass": t1, "efficiency_vs_1gpu": t1 / (c.ws * t_n),
+               "roofline_frac": (n * T_ / (t_n / 1e3)) / _roof(n, T_, w.f, sd, c.ws, True),
+               "steps": steps,
+               "parity": {"rows_checked": int(len(rows)),
+                          "within_1e-5": bool(np.all(np.abs(got - ref) <= tol)),
+                          "bit_exact_vs_oracle": bool(np.array_equal(got, ref)),
+                          "max_rel_err": float(np.max(np.abs(got - ref) /
+                                                      np.maximum(np.abs(ref), 1e-300)))}}
+    if sc is not None:
+        sc.close()
+    if full is not None:
+        full.close()
+    c.barrier()
+    return res
+
+
 def run_ours(args):
     import torch
     ws, rank, local = _dist()
+    if ws > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")     # rank counts in the log
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     # One GPU per rank.  TS_BENCH_BACKEND=gloo (flow tests only: several
     # independent instance-shard ranks on fewer GPUs, their kernels never wait
     # on one another) swaps the host-side barrier / max-reduce to gloo; the
@@ -254,6 +456,25 @@ def run_ours(args):
     e2e_s = max_over_ranks(time.perf_counter() - t0)
     e2e_value = w.n * T * e2e_steps * ws / e2e_s
     e2e_equal = bool(np.array_equal(host_out, gpu_scores))
+    del pinned, host_out
+
+    # ---- configs 4a (strong scaling) and 4b (tree sharding + NCCL reduce)
+    ctx = _Ctx(ws, rank, local, dev, backend, barrier, max_over_ranks)
+    subs = {}
+    if not args.no_sub:
+        del x, out
+        torch.cuda.empty_cache()
+        for name, fn in (("cfg4a", sub_cfg4a), ("cfg4b", sub_cfg4b)):
+            try:
+                subs[name] = fn(args, ctx)
+            except Exception as exc:  # noqa: BLE001
+                if ws > 1:     # the other ranks would wait in a collective forever
+                    import traceback
+                    traceback.print_exc()
+                    sys.stderr.flush()
+                    os._exit(1)
+                subs[name] = {"error": f"{type(exc).__name__}: {exc}"}
+            torch.cuda.empty_cache()
 
     if rank != 0:
         if ws > 1:
@@ -300,13 +521,10 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32 compare / f64 sum",
         "data": "synthetic (seeded; BASELINE cfg1 distributions)",
-        "config": {"workload": "cfg1: 1M x 136 mixed (ties), T=1000 complete d=8",
-                   "instances_per_gpu": w.n, "features": F, "trees": T, "depth": D,
-                   "parallelism": f"instance-sharded x{ws}",
-                   "l2": "inputs (544 MB/GPU) larger than L2; no flush",
-                   "kernel": f"{launches / max(1, args.steps):g} launch(es)/step: k_stream over the "
-                             "full waves of 128-row tiles + k_stream_ws on the last partial wave's rows; "
-                             "roofline.achieved is per step (both kernels)"},
+        "config": bench_config(ws),
+        "kernel": f"{launches / max(1, args.steps):g} launch(es)/step: k_stream over the "
+                  "full waves of 128-row tiles + k_stream_ws on the last partial wave's rows; "
+                  "roofline.achieved is per step (both kernels)",
         "roofline": roofline,
         "e2e": {"value": e2e_value, "unit": UNIT,
                 "h2d_bytes_per_step": w.n * F * 4, "d2h_bytes_per_step": w.n * 8,
@@ -315,6 +533,7 @@ def run_ours(args):
         "gpu_launches": launches,
         "clocks": clocks,
     }
+    line.update(subs)
     if ws == 1 and not args.no_cpu_baseline:
         cpu_val, rows, cpu_scores, threads, dt, passes = cpu_sample(w, args.cpu_seconds)
         line["cpu_baseline"] = {
@@ -340,12 +559,33 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sub", action="store_true",
+                    help="skip the config 4a / 4b sub-measurements")
+    ap.add_argument("--sub-steps", type=int, default=3)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch(args)
     return run_ours(args)
+
+
+def relaunch(args) -> int:
+    """``--gpus N`` without a launcher: run N ranks (one per GPU) under
+    torch.distributed.run on 127.0.0.1; rank 0 prints the JSON line."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
 
 
 if __name__ == "__main__":

@@ -194,6 +194,13 @@ int ts_nccl_comm_init(const void *id128, int nranks, int rank, int device, void 
 int ts_reduce_partials(void *comm, const double *partial, double *out, int64_t n, int root,
                        void *stream);
 int ts_nccl_comm_destroy(void *comm);
+/* Wait for the collectives enqueued on `stream`, polling
+ * ncclCommGetAsyncError meanwhile (SURVEY 5 failure detection): a peer or
+ * network failure aborts the communicator (ncclCommAbort, so the stream is
+ * released) and returns TS_ERR_CUDA with NCCL's message; so does a wait
+ * longer than timeout_ms (< 0: no limit).  ts_reduce_partials also checks
+ * the communicator's async state before and after enqueueing. */
+int ts_nccl_wait(void *comm, void *stream, int64_t timeout_ms);
 
 /* Host-buffer scoring: same argument meaning as the reference's generated
  * score_batch(x, n, f, out).  Copies x to the device in chunks on two

@@ -260,3 +260,41 @@ class COracle:
         lib.orc_score_linked(self.num_trees, _p(off), _p(fid), _p(val), _p(left), _p(right),
                              _p(w), _p(X), X.shape[0], X.shape[1], _p(out))
         return out
+
+
+# ---------------------------------------------------------------------------
+# sampled parity at BASELINE sizes (SURVEY 8(c) sampling protocol)
+# ---------------------------------------------------------------------------
+
+def sample_rows(n: int, k: int, run: int = 32, seed: int = 0) -> np.ndarray:
+    """Sorted row indices for a parity sample of about ``k`` rows spread over
+    ``[0, n)``: the first and last ``run`` rows (the tail tile included) plus
+    seeded random runs of ``run`` contiguous rows (whole 32-row warp blocks
+    when ``run`` is 32), so every region of a multi-GB matrix is visited."""
+    if n <= k:
+        return np.arange(n, dtype=np.int64)
+    rng = np.random.default_rng(seed)
+    starts = [0, max(0, n - run)]
+    starts += list(rng.integers(0, max(1, n - run), size=max(0, k // run - 2)))
+    rows = np.unique(np.concatenate([np.arange(s, min(n, s + run)) for s in starts]))
+    return rows.astype(np.int64)
+
+
+def runs_of(rows: np.ndarray):
+    """``[(start, length)]`` of the contiguous runs in sorted ``rows``."""
+    if len(rows) == 0:
+        return []
+    cut = np.flatnonzero(np.diff(rows) != 1) + 1
+    bounds = np.concatenate([[0], cut, [len(rows)]])
+    return [(int(rows[a]), int(b - a)) for a, b in zip(bounds[:-1], bounds[1:])]
+
+
+def score_tolerance(c: "COracle", X, ref) -> np.ndarray:
+    """Per-row bound of the north star's 1e-5 relative check with the
+    SURVEY 8(c) denominator guard: ``1e-5 * max(|s_ref|, sum_t |w_t leaf_t|)``."""
+    _, ords = c.score(X, with_ordinals=True)
+    mag = np.zeros(X.shape[0], np.float64)
+    for t in range(c.num_trees):
+        lv = c.cleaf[c.leaf_off[t]:c.leaf_off[t + 1]].astype(np.float64)
+        mag += np.abs(c.weight[t] * lv[ords[t]])
+    return 1e-5 * np.maximum(np.abs(ref), mag)

@@ -32,7 +32,7 @@ EXPORTS = ("ts_pack", "ts_pack_ex", "ts_trace", "ts_model_get_info", "ts_score",
            "ts_last_error", "ts_launch_count", "ts_version", "ts_synth_uniform", "ts_set_kernel_path",
            "ts_parse_model", "ts_flat_free", "ts_score_pipe", "ts_pipe_alloc", "ts_pipe_free",
            "ts_ipc_open", "ts_ipc_close", "ts_nccl_get_unique_id", "ts_nccl_comm_init",
-           "ts_reduce_partials", "ts_nccl_comm_destroy")
+           "ts_reduce_partials", "ts_nccl_comm_destroy", "ts_nccl_wait")
 
 
 class NativeLibraryError(RuntimeError):
@@ -158,6 +158,7 @@ def load(build_if_missing: bool = True):
                                           ctypes.POINTER(P)]
         lib.ts_reduce_partials.argtypes = [P, P, P, I64, ctypes.c_int, P]
         lib.ts_nccl_comm_destroy.argtypes = [P]
+        lib.ts_nccl_wait.argtypes = [P, P, I64]
         for name in EXPORTS:
             getattr(lib, name)
         _lib = lib

@@ -284,7 +284,12 @@ cudaError_t launch_stream(int D, const StreamArgs &a0, int device, cudaStream_t 
     if (!pool) return stream_detail::kStreamTable[D](a, device, stream);
     double *scratch = nullptr;
     cudaError_t e = cudaMallocFromPoolAsync((void **)&scratch, scratch_bytes, pool, stream);
-    if (e != cudaSuccess) return e;
+    if (e != cudaSuccess) {
+        // out of memory for the split's scratch: the one-pass kernel needs
+        // none and gives the same bits, only slower for this batch size
+        (void)cudaGetLastError();
+        return stream_detail::kStreamTable[D](a, device, stream);
+    }
     StreamArgs w = a;
     w.splits = splits;
     w.leaf_out = scratch;

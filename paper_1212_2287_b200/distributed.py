@@ -44,6 +44,13 @@ import numpy as np
 from .model import FlatModel
 
 
+def _global(group, r: int) -> int:
+    """Global rank of ``group``'s rank ``r`` (torch's collectives and
+    send/recv take global ranks even when a subgroup is passed)."""
+    import torch.distributed as dist
+    return dist.get_global_rank(group, r) if group is not None else r
+
+
 def row_shard(n: int, world: int, rank: int) -> tuple[int, int]:
     """Contiguous rows ``[a, b)`` of rank ``rank`` (sizes differ by at most 1)."""
     return n * rank // world, n * (rank + 1) // world
@@ -161,8 +168,31 @@ class ShardedScorer:
         self.plan = plan(mode, n_total, flat, self.world, self.rank, depths)
         shard = flat if mode == "instance" else flat.subset(*self.plan.trees)
         self.score = (make_scorer or (lambda fm: gpu_scorer(fm, device)))(shard)
+        # gloo moves CPU tensors only: CUDA payloads are staged through the host
+        self._stage = dist.get_backend(group) == "gloo"
+        # tree-reduce on GPUs over NCCL goes through the C ABI's own reduction
+        # (ts_reduce_partials, with async-error polling); other backends and
+        # the CPU test scorers use torch.distributed
+        self.reducer = None
+        if mode == "tree-reduce" and make_scorer is None and not self._stage:
+            import torch
+            dev = torch.cuda.current_device() if device is None else int(device)
+            self.reducer = NcclReducer(dev, group)
         if mode == "tree-p2p":
             self._setup_p2p(device)
+
+    def _send(self, t, dst):
+        import torch.distributed as dist
+        dist.send(t.cpu() if self._stage and t.is_cuda else t, dst=dst, group=self.group)
+
+    def _recv(self, t, src):
+        import torch.distributed as dist
+        if self._stage and t.is_cuda:
+            h = t.cpu()
+            dist.recv(h, src=src, group=self.group)
+            t.copy_(h)
+        else:
+            dist.recv(t, src=src, group=self.group)
 
     def _setup_p2p(self, device):
         """Allocate this rank's receive buffers, publish their IPC handles and
@@ -195,7 +225,17 @@ class ShardedScorer:
             out = torch.empty(self.n_total, dtype=torch.float64, device=dev)
         if mode == "tree-reduce":
             self.score(x_local, out, False)
-            dist.reduce(out, dst=0, op=dist.ReduceOp.SUM, group=grp)
+            # scores land on the GROUP's rank 0
+            if self.reducer is not None:
+                self.reducer.reduce(out, out)          # in place on the root
+                self.reducer.wait()
+            elif self._stage and out.is_cuda:
+                h = out.cpu()
+                dist.reduce(h, dst=_global(grp, 0), op=dist.ReduceOp.SUM, group=grp)
+                if rank == 0:
+                    out.copy_(h)
+            else:
+                dist.reduce(out, dst=_global(grp, 0), op=dist.ReduceOp.SUM, group=grp)
             return out
         if mode == "tree-p2p":
             return self._call_p2p(x_local, out)
@@ -206,10 +246,10 @@ class ShardedScorer:
             c1 = min(self.n_total, c0 + self.chunk_rows)
             seg = out[c0:c1]
             if rank > 0:
-                dist.recv(seg, src=rank - 1, group=grp)
+                self._recv(seg, _global(grp, rank - 1))
             self.score(x_local[c0:c1], seg, rank > 0)
             if rank < world - 1:
-                dist.send(seg, dst=rank + 1, group=grp)
+                self._send(seg, _global(grp, rank + 1))
         return out
 
 
@@ -238,7 +278,8 @@ class ShardedScorer:
         return out
 
     def close(self):
-        for b in (getattr(self, "recv", None), getattr(self, "send", None)):
+        for b in (getattr(self, "recv", None), getattr(self, "send", None),
+                  getattr(self, "reducer", None)):
             if b is not None:
                 b.close()
 
@@ -258,8 +299,7 @@ class NcclReducer:
         if self.rank == 0 and lib.ts_nccl_get_unique_id(uid) != _lib.TS_OK:
             raise RuntimeError(f"ts_nccl_get_unique_id: {_lib.last_error()}")
         box = [uid.raw if self.rank == 0 else None]
-        dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0)
-                                   if group is not None else 0, group=group)
+        dist.broadcast_object_list(box, src=_global(group, 0), group=group)
         uid = ctypes.create_string_buffer(box[0], 128)
         comm = ctypes.c_void_p()
         if lib.ts_nccl_comm_init(uid, self.world, self.rank, int(device),
@@ -281,6 +321,18 @@ class NcclReducer:
         if rc != _lib.TS_OK:
             raise RuntimeError(f"ts_reduce_partials: {_lib.last_error()}")
         return out
+
+    def wait(self, timeout_ms: int = 60_000):
+        """Block until the reduction on the current stream finished, polling
+        NCCL's async error state (``ts_nccl_wait``): a dead peer or a timeout
+        aborts the communicator and raises instead of hanging."""
+        import ctypes
+        import torch
+        from . import _lib
+        stream = torch.cuda.current_stream().cuda_stream
+        rc = self._lib.ts_nccl_wait(self.comm, ctypes.c_void_p(stream), int(timeout_ms))
+        if rc != _lib.TS_OK:
+            raise RuntimeError(f"ts_nccl_wait: {_lib.last_error()}")
 
     def close(self):
         if getattr(self, "comm", None) is not None and self.comm.value:
@@ -305,7 +357,7 @@ def gather_scores(local, n_total: int, group=None, dst: int = 0):
     buf = torch.zeros(width, dtype=torch.float64, device=local.device)
     buf[:local.shape[0]] = local
     parts = [torch.empty_like(buf) for _ in range(world)] if rank == dst else None
-    dist.gather(buf, parts, dst=dst, group=group)
+    dist.gather(buf, parts, dst=_global(group, dst), group=group)
     if rank != dst:
         return None
     return torch.cat([parts[r][:b - a] for r, (a, b) in enumerate(sizes)])

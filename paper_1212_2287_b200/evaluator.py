@@ -124,6 +124,32 @@ class GpuModel:
         self.num_trees = int(flat.num_trees)
         self.node_count = int(flat.tree_off[-1])  # logical nodes (internal + leaves)
 
+    def _check_x(self, x, what="x"):
+        torch = _torch()
+        if x.dim() != 2 or x.dtype != torch.float32 or not x.is_cuda:
+            raise TypeError(f"{what} must be a 2-D float32 CUDA tensor")
+        if x.stride(1) != 1:
+            raise ValueError(f"{what} rows must be contiguous (stride(1) == 1)")
+        if x.device.index != self.device:
+            # the kernel runs on the model's GPU: another GPU's pointer would
+            # fault there (no peer mapping) and poison the whole context
+            raise ValueError(f"{what} is on cuda:{x.device.index}, the model on cuda:{self.device}")
+
+    def _check_buf(self, t, what, dtype, n):
+        """Device buffers the kernel writes: right dtype, device, contiguity
+        and at least ``n`` elements (a short or mistyped buffer would be
+        overrun on the device)."""
+        if t is None:
+            return
+        if not t.is_cuda or t.device.index != self.device:
+            raise ValueError(f"{what} must be a CUDA tensor on cuda:{self.device}")
+        if t.dtype != dtype:
+            raise ValueError(f"{what} must have dtype {dtype}, got {t.dtype}")
+        if not t.is_contiguous():
+            raise ValueError(f"{what} must be contiguous")
+        if t.numel() < n:
+            raise ValueError(f"{what} has {t.numel()} elements, needs >= {n}")
+
     def score(self, x, out=None, ordinals=None, status=None, stream=None, accumulate=False):
         """Enqueue scoring of a CUDA float32 ``[n, f]`` tensor (row stride >= f).
 
@@ -136,21 +162,23 @@ class GpuModel:
         (a tree shard); scoring continues from it (``ts_score_ex``).
         """
         torch = _torch()
-        if x.dim() != 2 or x.dtype != torch.float32 or not x.is_cuda:
-            raise TypeError("x must be a 2-D float32 CUDA tensor")
-        if x.stride(1) != 1:
-            raise ValueError("x rows must be contiguous (stride(1) == 1)")
+        self._check_x(x)
         n, f = x.shape
         if f != self.num_features:
             raise ValueError(f"dataset has shape {tuple(x.shape)}, expected (n, {self.num_features})")
         if out is None:
             out = torch.empty(n, dtype=torch.float64, device=x.device)
+        self._check_buf(out, "out", torch.float64, n)
+        self._check_buf(status, "status", torch.int32, 1)
         ld_ord = 0
         ord_ptr = None
         if ordinals is not None:
             if ordinals.element_size() != 2 or ordinals.dim() != 2 or ordinals.stride(1) != 1 \
-                    or ordinals.shape[0] != self.num_trees or ordinals.shape[1] < n:
-                raise ValueError("ordinals must be a [T, >=n] 16-bit row-major tensor")
+                    or ordinals.shape[0] != self.num_trees or ordinals.shape[1] < n \
+                    or ordinals.is_floating_point():
+                raise ValueError("ordinals must be a [T, >=n] 16-bit integer row-major tensor")
+            if not ordinals.is_cuda or ordinals.device.index != self.device:
+                raise ValueError(f"ordinals must be a CUDA tensor on cuda:{self.device}")
             ld_ord = ordinals.stride(0)
             ord_ptr = ctypes.c_void_p(ordinals.data_ptr())
         if stream is None:
@@ -177,11 +205,13 @@ class GpuModel:
         writes ``out``).  ``epoch`` must grow by one per call.
         """
         torch = _torch()
-        if x.dim() != 2 or x.dtype != torch.float32 or not x.is_cuda or x.stride(1) != 1:
-            raise TypeError("x must be a row-major 2-D float32 CUDA tensor")
+        self._check_x(x)
         n, f = x.shape
+        if f != self.num_features:
+            raise ValueError(f"dataset has shape {tuple(x.shape)}, expected (n, {self.num_features})")
         if out is None:
             out = torch.empty(n, dtype=torch.float64, device=x.device)
+        self._check_buf(out, "out", torch.float64, n)
         if stream is None:
             stream = torch.cuda.current_stream(x.device)
         pipe = _lib.Pipe(sums_in or None, flags_in or None, sums_out or None, flags_out or None,
@@ -197,8 +227,19 @@ class GpuModel:
     def trace(self, x, out=None, leaf_ord=None, visited=None, stream=None):
         """``ts_trace`` on a CUDA float32 ``[n, f]`` tensor (model packed with trace=True)."""
         torch = _torch()
+        self._check_x(x)
         n, f = x.shape
+        if f != self.num_features:
+            raise ValueError(f"dataset has shape {tuple(x.shape)}, expected (n, {self.num_features})")
         words = (self.num_features + 31) // 32
+        self._check_buf(out, "out", torch.float64, n)
+        self._check_buf(visited, "visited", torch.int32, n * words)
+        if leaf_ord is not None:
+            if leaf_ord.element_size() != 2 or leaf_ord.dim() != 2 or leaf_ord.stride(1) != 1 \
+                    or leaf_ord.shape[0] != self.num_trees or leaf_ord.shape[1] < n:
+                raise ValueError("leaf_ord must be a [T, >=n] 16-bit row-major tensor")
+            if not leaf_ord.is_cuda or leaf_ord.device.index != self.device:
+                raise ValueError(f"leaf_ord must be a CUDA tensor on cuda:{self.device}")
         if stream is None:
             stream = torch.cuda.current_stream(x.device)
         p = lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None

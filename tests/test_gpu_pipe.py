@@ -147,6 +147,7 @@ def _reduce_worker(rank, world, port, q):
         red = NcclReducer(0)
         part = torch.arange(1000, dtype=torch.float64, device="cuda") * 0.5
         out = red.reduce(part)
+        red.wait(timeout_ms=60_000)       # polls ncclCommGetAsyncError
         torch.cuda.synchronize()
         red.close()
         dist.destroy_process_group()

@@ -132,7 +132,14 @@ def main():
         got = out.cpu().numpy()[rows]
         host = np.concatenate([w.rows(int(r), 1) for r in rows]) if w.x is None \
             else w.x[rows]
-        ref = oracle.COracle(w.flat.arrays()).score(host)
+        ref, ref_ord = oracle.COracle(w.flat.arrays()).score(host, with_ordinals=True)
+        # per-tree ordinals of the same sample (re-scored as one small batch,
+        # whose scores must equal the full pass's at those rows)
+        idx = torch.from_numpy(rows).to(dev)
+        xs = x.index_select(0, idx)
+        ords = torch.empty((T, len(rows)), dtype=torch.int16, device=dev)
+        s_sample = ev.model.score(xs, ordinals=ords).cpu().numpy()
+        o_sample = ords.cpu().numpy().view(np.uint16)
         line = {"config": key, "workload": w.name, "n": w.n, "f": w.f, "trees": T,
                 "sum_depth": info["sum_depth"], "segments": info["num_segments"],
                 "complete_trees": info["complete_trees"], "compact_trees": info["compact_trees"],
@@ -140,6 +147,8 @@ def main():
                 "roofline_bound": "issue" if t_issue > t_hbm else "hbm",
                 "roofline_evals_per_s": roof, "roofline_frac": evals / roof,
                 "parity_rows": int(len(rows)), "bit_exact": bool(np.array_equal(got, ref)),
+                "ordinals_bit_exact": bool(np.array_equal(o_sample, ref_ord)),
+                "sample_rescore_equal": bool(np.array_equal(s_sample, got)),
                 "max_abs_err": float(np.max(np.abs(got - ref))), "gen_s": gen_s,
                 "timing": timing}
         print(json.dumps(line), flush=True)
