@@ -160,6 +160,65 @@ def cpu_sample(w, target_s: float, threads: int | None = None):
     return rows * T * passes / dt, rows, scores, threads, dt, passes
 
 
+def generated_sample(w, target_s: float, threads: int):
+    """The reference's CodeGen strategy on the same workload, when its unit was
+    prebuilt (``__graft_entry__.build`` compiles config 1's 50 MB of generated
+    C, ~100 s): the C text of ref ``codegen.emit_source`` (byte-identical,
+    ``oracle/codegen.py``) compiled with its flags, one thread per core over
+    row shards.  Gated on the 1,000-row prefix against the C oracle first
+    (ref bench.py:220-231).  Returns (evals/s, rows, seconds, passes) or None."""
+    import oracle
+    from oracle import codegen
+    unit = codegen.cached_unit(w.flat)
+    if unit is None:
+        return None
+    prefix = w.x[:1000]
+    if not np.array_equal(unit.score(prefix, threads=threads),
+                          oracle.COracle(w.flat.arrays()).score(prefix, threads=threads)):
+        raise RuntimeError("generated CPU baseline failed the 1000-row correctness gate")
+    out = np.empty(w.n, np.float64)
+    probe = min(w.n, 2000)
+    t0 = time.perf_counter()
+    unit.score_parallel(w.x[:probe], out[:probe], threads)
+    dt = time.perf_counter() - t0
+    rows = int(min(w.n, max(probe, probe * target_s / max(dt, 1e-6))))
+    passes, t0 = 0, time.perf_counter()
+    while True:
+        unit.score_parallel(w.x[:rows], out[:rows], threads)
+        passes += 1
+        dt = time.perf_counter() - t0
+        if dt >= target_s or passes >= 50:
+            break
+    return rows * T * passes / dt, rows, dt, passes
+
+
+def cpu_baseline_line(w, target_s: float):
+    """the faster of the reference's VPred path (C port) and
+    its CodeGen strategy (its own generated C), both on all host cores.
+    Returns (cpu_baseline dict, port scores of the prefix, prefix rows)."""
+    cpu_val, rows, cpu_scores, threads, dt, passes = cpu_sample(w, target_s)
+    port = {"value": cpu_val, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{passes} pass(es) over the first {rows} rows x {T} trees ({dt:.1f} s; "
+                      "C restatement of the reference VPred path, oracle/ts_oracle.c, "
+                      "lockstep batches of 64)"}
+    gen = generated_sample(w, min(target_s, 4.0), threads)
+    if gen is None:
+        port["candidates"] = {"port": cpu_val, "generated": "not prebuilt (oracle/_gen)"}
+        return port, cpu_scores, rows
+    g_val, g_rows, g_dt, g_passes = gen
+    cand = {"port": cpu_val, "generated": g_val,
+            "generated_sample": f"{g_passes} pass(es) over the first {g_rows} rows x {T} trees "
+                                f"({g_dt:.1f} s; the reference's generated C, -O3, "
+                                f"{threads} threads over row shards)"}
+    if g_val > cpu_val:
+        line = {"value": g_val, "unit": UNIT, "cores": threads, "kind": "reference",
+                "sample": cand["generated_sample"]}
+    else:
+        line = port
+    line["candidates"] = cand
+    return line, cpu_scores, rows
+
+
 def run_reference(args):
     ws, rank, _ = _dist()
     if rank != 0:
@@ -169,18 +228,37 @@ def run_reference(args):
     import oracle
     c = oracle.COracle(w.flat.arrays())
     threads = len(os.sched_getaffinity(0))
-    # size each step so the whole run stays within ~3 minutes
-    per_step = max(0.5, min(3.0, 150.0 / max(1, args.steps + args.warmup)))
+    # the faster of the VPred port and the reference's own
+    # generated C (when prebuilt) is the reference arm
+    gen = generated_sample(w, 3.0, threads)
     probe = 2000
     t0 = time.perf_counter()
     c.score(w.x[:probe], threads=threads)
+    port_rate = probe * T / max(time.perf_counter() - t0, 1e-9)
+    use_gen = gen is not None and gen[0] > port_rate
+    if use_gen:
+        from oracle import codegen
+        unit = codegen.cached_unit(w.flat)
+        buf = np.empty(w.n, np.float64)
+
+        def score(xx):
+            unit.score_parallel(xx, buf[:len(xx)], threads)
+        kind, what = "reference", "the reference's generated C (CodeGen strategy), -O3"
+    else:
+        def score(xx):
+            c.score(xx, threads=threads)
+        kind, what = "port", "C restatement of the reference VPred path, oracle/ts_oracle.c, v=64"
+    # size each step so the whole run stays within ~3 minutes
+    per_step = max(0.5, min(3.0, 150.0 / max(1, args.steps + args.warmup)))
+    t0 = time.perf_counter()
+    score(w.x[:probe])
     rows = int(min(w.n, max(probe, probe * per_step / max(time.perf_counter() - t0, 1e-6))))
     for s in range(args.warmup):
-        c.score(w.x[:rows], threads=threads)
+        score(w.x[:rows])
     t0 = time.perf_counter()
     for s in range(args.steps):
         off = (s * rows) % max(1, w.n - rows)
-        c.score(w.x[off:off + rows], threads=threads)
+        score(w.x[off:off + rows])
     dt = time.perf_counter() - t0
     value = rows * T * args.steps / dt
     line = {
@@ -189,9 +267,10 @@ def run_reference(args):
         "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32 compare / f64 sum", "data": "synthetic",
         "config": bench_config(max(ws, args.gpus)),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{rows} rows x {T} trees per step (C restatement of the "
-                                   "reference VPred path, oracle/ts_oracle.c, v=64)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
+                         "sample": f"{rows} rows x {T} trees per step ({what})",
+                         "candidates": {"port_probe": port_rate,
+                                        "generated": gen[0] if gen else "not prebuilt"}},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -535,12 +614,7 @@ def run_ours(args):
     }
     line.update(subs)
     if ws == 1 and not args.no_cpu_baseline:
-        cpu_val, rows, cpu_scores, threads, dt, passes = cpu_sample(w, args.cpu_seconds)
-        line["cpu_baseline"] = {
-            "value": cpu_val, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"{passes} pass(es) over the first {rows} rows x {T} trees ({dt:.1f} s; "
-                      "C restatement of the reference VPred path, oracle/ts_oracle.c, "
-                      "lockstep batches of 64)"}
+        line["cpu_baseline"], cpu_scores, rows = cpu_baseline_line(w, args.cpu_seconds)
         line["parity"] = {"rows_checked": rows,
                           "bit_exact_vs_oracle": bool(np.array_equal(cpu_scores,
                                                                      gpu_scores[:rows]))}
