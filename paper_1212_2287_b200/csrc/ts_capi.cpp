@@ -347,6 +347,35 @@ class CopyPool {
 
 }  // namespace
 
+// A HostScratch for the duration of one ts_score_host call: concurrent host
+// callers sharing a model each get their own streams and buffers (created on
+// first need, up to ts_model::kMaxHostScratch, then waited for).
+struct ScratchLease {
+    ts_model *m;
+    HostScratch *s;
+    explicit ScratchLease(ts_model *mm) : m(mm) {
+        std::unique_lock<std::mutex> l(m->scratch_mu);
+        m->scratch_cv.wait(l, [&] {
+            return !m->scratch_free.empty() ||
+                   (int)m->scratch_all.size() < ts_model::kMaxHostScratch;
+        });
+        if (!m->scratch_free.empty()) {
+            s = m->scratch_free.back();
+            m->scratch_free.pop_back();
+        } else {
+            m->scratch_all.emplace_back(new HostScratch());
+            s = m->scratch_all.back().get();
+        }
+    }
+    ~ScratchLease() {
+        {
+            std::lock_guard<std::mutex> l(m->scratch_mu);
+            m->scratch_free.push_back(s);
+        }
+        m->scratch_cv.notify_one();
+    }
+};
+
 extern "C" int ts_score_host(const ts_model *mc, const float *x, int64_t n, int64_t f,
                              double *out) {
     int rc = check_args(mc, x, n, f, f, out);
@@ -355,8 +384,8 @@ extern "C" int ts_score_host(const ts_model *mc, const float *x, int64_t n, int6
     ts_model *m = const_cast<ts_model *>(mc);
     DeviceGuard g(m->device);
     if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
-    std::lock_guard<std::mutex> lock(m->scratch_mu);
-    HostScratch &s = m->scratch;
+    ScratchLease lease(m);
+    HostScratch &s = *lease.s;
     // Chunk so that H2D of chunk i+1 overlaps the scoring of chunk i (and,
     // for pageable input, the staging copy of chunk i+1 overlaps the DMA of
     // chunk i): 64 MB chunks, but at least four of them once the batch is
@@ -507,26 +536,28 @@ extern "C" void ts_free(ts_model *m) {
     {
         DeviceGuard g(m->device);
         free_tables(&m->dev);
-        HostScratch &s = m->scratch;
-        if (s.copy) {
-            cudaStreamSynchronize(s.copy);
-            cudaStreamSynchronize(s.compute);
+        for (auto &sp : m->scratch_all) {
+            HostScratch &s = *sp;
+            if (s.copy) {
+                cudaStreamSynchronize(s.copy);
+                cudaStreamSynchronize(s.compute);
+            }
+            cudaFree(s.x[0]);
+            cudaFree(s.x[1]);
+            cudaFree(s.out);
+            cudaFree(s.status);
+            cudaFreeHost(s.hx[0]);
+            cudaFreeHost(s.hx[1]);
+            cudaFreeHost(s.hout[0]);
+            cudaFreeHost(s.hout[1]);
+            for (int i = 0; i < 2; i++) {
+                if (s.copied[i]) cudaEventDestroy(s.copied[i]);
+                if (s.consumed[i]) cudaEventDestroy(s.consumed[i]);
+                if (s.d2h[i]) cudaEventDestroy(s.d2h[i]);
+            }
+            if (s.copy) cudaStreamDestroy(s.copy);
+            if (s.compute) cudaStreamDestroy(s.compute);
         }
-        cudaFree(s.x[0]);
-        cudaFree(s.x[1]);
-        cudaFree(s.out);
-        cudaFree(s.status);
-        cudaFreeHost(s.hx[0]);
-        cudaFreeHost(s.hx[1]);
-        cudaFreeHost(s.hout[0]);
-        cudaFreeHost(s.hout[1]);
-        for (int i = 0; i < 2; i++) {
-            if (s.copied[i]) cudaEventDestroy(s.copied[i]);
-            if (s.consumed[i]) cudaEventDestroy(s.consumed[i]);
-            if (s.d2h[i]) cudaEventDestroy(s.d2h[i]);
-        }
-        if (s.copy) cudaStreamDestroy(s.copy);
-        if (s.compute) cudaStreamDestroy(s.compute);
     }
     delete m;
 }

@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <condition_variable>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -142,8 +144,14 @@ struct ts_model {
     std::vector<ts::Segment> segments;
     ts::DeviceTables dev;
     ts_model_info info{};
+    // Host-buffer pipelines (ts_score_host): one HostScratch (streams, device
+    // chunks, pinned staging) per concurrent caller, reused across calls;
+    // callers beyond kMaxHostScratch wait for one to come back.
+    static constexpr int kMaxHostScratch = 8;
     std::mutex scratch_mu;
-    ts::HostScratch scratch;
+    std::condition_variable scratch_cv;
+    std::vector<std::unique_ptr<ts::HostScratch>> scratch_all;
+    std::vector<ts::HostScratch *> scratch_free;
 };
 
 namespace ts {

@@ -815,3 +815,41 @@ def test_wave_tail_on_warp_split_kernel(d):
         s, o = oracle.COracle(model.arrays()).score(x, threads=8, with_ordinals=True)
         assert np.array_equal(ev.predict_batch(x), s)
         assert np.array_equal(ev.leaf_indices(x), o.astype(np.int64))
+
+
+def test_concurrent_host_pipelines_overlap():
+    """Host-buffer calls sharing one model run their chunked H2D/score/D2H
+    pipelines concurrently (one HostScratch lease per caller, ts_capi.cpp
+    ScratchLease), each bit-exact: 6 threads, multi-chunk batches (> 16 MB,
+    pageable and pinned inputs)."""
+    import threading
+    import torch
+    from paper_1212_2287_b200.synth import complete_flat
+    rng = np.random.default_rng(11)
+    T, d, F = 50, 6, 136
+    n_int = (1 << d) - 1
+    flat = complete_flat(F, d, rng.integers(0, F, (T, n_int)), rng.random((T, n_int)),
+                         rng.standard_normal((T, 1 << d)))
+    ev = _ev(flat)
+    ref = oracle.COracle(flat.arrays())
+    xs = [rng.random((40_000 + 997 * i, F), dtype=np.float32) for i in range(6)]
+    xs[1] = torch.from_numpy(xs[1]).pin_memory().numpy()
+    want = [ref.score(x, threads=4) for x in xs]
+    errors = []
+    barrier = threading.Barrier(len(xs))
+
+    def worker(i):
+        try:
+            barrier.wait()
+            for _ in range(3):
+                if not np.array_equal(ev.predict_batch(xs[i]), want[i]):
+                    errors.append(i)
+        except Exception as e:  # noqa: BLE001
+            errors.append((i, repr(e)))
+
+    ts_ = [threading.Thread(target=worker, args=(i,)) for i in range(len(xs))]
+    for t in ts_:
+        t.start()
+    for t in ts_:
+        t.join()
+    assert errors == []
