@@ -109,10 +109,11 @@ struct DeviceGuard {
 int score_device(const ts_model *m, const float *x, int64_t n, int64_t f, int64_t ld,
                  double *out, uint16_t *ord, int64_t ld_ord, int32_t *status,
                  cudaStream_t stream, bool accumulate = false,
-                 const PipeArgs *pipe = nullptr) {
+                 const PipeArgs *pipe = nullptr, bool x_mapped = false) {
     if (n == 0) return TS_OK;
     ScoreArgs a{};
     a.x = x;
+    a.x_mapped = x_mapped ? 1 : 0;
     a.n = n;
     a.ld = ld;
     a.F = m->num_features;
@@ -347,6 +348,61 @@ class CopyPool {
 
 }  // namespace
 
+// Small batches: rows copied into mapped pinned memory, which the scoring
+// kernel reads over PCIe (as its own staging loads); scores and the
+// non-finite flag written straight back into mapped memory; one launch and
+// one stream synchronisation per call instead of memset + H2D + kernel +
+// two D2H commands (each ~2-5 us of command latency at this size).
+constexpr int64_t kDirectBytes = 1 << 20;
+
+int score_host_direct(ts_model *m, HostScratch &s, const float *x, int64_t n, int64_t f,
+                      double *out) {
+    const size_t xb = ((size_t)n * f * sizeof(float) + 255) & ~(size_t)255;
+    const size_t need = xb + (((size_t)n * sizeof(double) + 255) & ~(size_t)255) + 256;
+    cudaError_t e;
+    if (s.map_bytes < need) {
+        if (s.map) cudaFreeHost(s.map);
+        s.map = nullptr;
+        s.map_bytes = 0;
+        const size_t cap = std::max<size_t>(need, 16 << 10);
+        if ((e = cudaHostAlloc((void **)&s.map, cap, cudaHostAllocMapped)))
+            return cuda_fail(e, "cudaHostAlloc(mapped)");
+        s.map_bytes = cap;
+    }
+    unsigned char *dmap = nullptr;
+    if ((e = cudaHostGetDevicePointer((void **)&dmap, s.map, 0)))
+        return cuda_fail(e, "cudaHostGetDevicePointer");
+    float *hx = reinterpret_cast<float *>(s.map);
+    double *hout = reinterpret_cast<double *>(s.map + xb);
+    volatile int32_t *hstatus = reinterpret_cast<int32_t *>(s.map + s.map_bytes - 256);
+    // rows already in page-locked (mapped) memory are read in place; others
+    // are copied into the mapped buffer (a small copy: below 64 KB the
+    // pointer query costs more than it saves)
+    const float *dx = reinterpret_cast<const float *>(dmap);
+    const size_t in_bytes = (size_t)n * f * sizeof(float);
+    void *dpin = nullptr;
+    if (in_bytes > (64u << 10) && host_pinned(x) &&
+        cudaHostGetDevicePointer(&dpin, const_cast<float *>(x), 0) == cudaSuccess && dpin)
+        dx = static_cast<const float *>(dpin);
+    else {
+        (void)cudaGetLastError();
+        CopyPool::get().copy(hx, x, in_bytes);
+    }
+    *hstatus = 0;
+    int rc = score_device(m, dx, n, f, f,
+                          reinterpret_cast<double *>(dmap + xb), nullptr, 0,
+                          reinterpret_cast<int32_t *>(dmap + s.map_bytes - 256), s.compute,
+                          false, nullptr, true);
+    if (rc) {
+        cudaStreamSynchronize(s.compute);
+        return rc;
+    }
+    if ((e = cudaStreamSynchronize(s.compute))) return cuda_fail(e, "direct host path (sync)");
+    memcpy(out, hout, (size_t)n * sizeof(double));
+    if (*hstatus) return fail(TS_ERR_NONFINITE, "dataset contains non-finite values");
+    return TS_OK;
+}
+
 // A HostScratch for the duration of one ts_score_host call: concurrent host
 // callers sharing a model each get their own streams and buffers (created on
 // first need, up to ts_model::kMaxHostScratch, then waited for).
@@ -386,6 +442,14 @@ extern "C" int ts_score_host(const ts_model *mc, const float *x, int64_t n, int6
     if (g.err != cudaSuccess) return cuda_fail(g.err, "cudaSetDevice");
     ScratchLease lease(m);
     HostScratch &s = *lease.s;
+    cudaError_t e = cudaSuccess;
+    if (!s.compute) {
+        if ((e = cudaStreamCreateWithFlags(&s.copy, cudaStreamNonBlocking)) ||
+            (e = cudaStreamCreateWithFlags(&s.compute, cudaStreamNonBlocking)))
+            return cuda_fail(e, "cudaStreamCreate");
+    }
+    const int64_t in_bytes = n * f * (int64_t)sizeof(float);
+    if (in_bytes <= kDirectBytes) return score_host_direct(m, s, x, n, f, out);
     // Chunk so that H2D of chunk i+1 overlaps the scoring of chunk i (and,
     // for pageable input, the staging copy of chunk i+1 overlaps the DMA of
     // chunk i): 64 MB chunks, but at least four of them once the batch is
@@ -403,11 +467,7 @@ extern "C" int ts_score_host(const ts_model *mc, const float *x, int64_t n, int6
     // (a cudaMemcpyAsync from pageable memory would stage synchronously at
     // ~10 GB/s); results land in pinned memory and are copied out on the host.
     const bool x_pinned = host_pinned(x), out_pinned = host_pinned(out);
-    cudaError_t e = cudaSuccess;
-    if (!s.copy) {
-        if ((e = cudaStreamCreateWithFlags(&s.copy, cudaStreamNonBlocking)) ||
-            (e = cudaStreamCreateWithFlags(&s.compute, cudaStreamNonBlocking)))
-            return cuda_fail(e, "cudaStreamCreate");
+    if (!s.copied[0]) {
         for (int i = 0; i < 2; i++) {
             if ((e = cudaEventCreateWithFlags(&s.copied[i], cudaEventDisableTiming)) ||
                 (e = cudaEventCreateWithFlags(&s.consumed[i], cudaEventDisableTiming)) ||
@@ -557,6 +617,7 @@ extern "C" void ts_free(ts_model *m) {
             }
             if (s.copy) cudaStreamDestroy(s.copy);
             if (s.compute) cudaStreamDestroy(s.compute);
+            if (s.map) cudaFreeHost(s.map);
         }
     }
     delete m;

@@ -132,6 +132,11 @@ struct HostScratch {
     double *hout[2] = {nullptr, nullptr};
     int64_t hx_rows = 0, hout_rows = 0;
     cudaEvent_t d2h[2] = {nullptr, nullptr};
+    // small batches (ts_score_host direct path): mapped pinned memory the
+    // kernel reads rows from and writes scores and status into over PCIe,
+    // so a call is one launch and one stream sync (no copy commands)
+    unsigned char *map = nullptr;   // rows | scores | status
+    size_t map_bytes = 0;
 };
 
 }  // namespace ts
@@ -187,6 +192,10 @@ struct ScoreArgs {
     long long ld_ord;
     int32_t *status;
     PipeArgs pipe;  // k_stream only (ts_score_pipe)
+    // x is mapped pinned HOST memory (ts_score_host's small-batch path):
+    // kernels that stage each row once read it over PCIe; the others get a
+    // device copy first (x_device_copy)
+    int x_mapped;
 };
 
 // Arguments of the shared-memory streaming kernel (ts_stream.cu).
@@ -224,6 +233,7 @@ struct StreamArgs {
     uint32_t lb_bytes;  // warp-split kernel (k_stream_ws): two tpc x 32 fp32 leaf buffers
     int ws_ctas;        // warp-split kernel: CTAs per SM (2 or 3)
     int k;              // k_stream lockstep chains per thread (chains_for_depth / _fallback)
+    int x_mapped;       // see ScoreArgs::x_mapped
 };
 // n: rows of the launch (-1 at pack time: shape-independent checks only).
 bool plan_stream(int F, int D, int device, StreamArgs *a, long long n = -1);
@@ -232,6 +242,10 @@ bool plan_stream(int F, int D, int device, StreamArgs *a, long long n = -1);
 bool plan_stream_ws(int F, int D, int device, StreamArgs *a);
 inline int split_fid_width(int F) { return F <= 256 ? 1 : 2; }
 cudaError_t launch_stream(int D, const StreamArgs &a, int device, cudaStream_t stream);
+// Stream-ordered device copy of rows [0, n) x ld of (mapped host) x from the
+// library's memory pool; *dst is nullptr (and cudaSuccess) if no pool.
+cudaError_t x_device_copy(const float *x, long long n, long long ld, int device,
+                          cudaStream_t stream, float **dst);
 
 // Irregular-tree streaming kernel (ts_cstream.cu).
 constexpr int kCStreamMaxT = 64;     // tree slots per chunk

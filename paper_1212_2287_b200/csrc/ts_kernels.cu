@@ -268,9 +268,45 @@ const LaunchFn kCompleteTable[TS_MAX_DEPTH + 1] = {
 
 }  // namespace
 
-cudaError_t launch_segment(const Segment &seg, const ScoreArgs &args, int device,
+cudaError_t x_device_copy(const float *x, long long n, long long ld, int device,
+                          cudaStream_t stream, float **dst) {
+    *dst = nullptr;
+    cudaMemPool_t pool = scratch_pool(device);
+    if (!pool) return cudaSuccess;
+    const size_t bytes = (size_t)n * ld * sizeof(float);
+    cudaError_t e = cudaMallocFromPoolAsync((void **)dst, bytes, pool, stream);
+    if (e != cudaSuccess) {
+        *dst = nullptr;
+        return e;
+    }
+    e = cudaMemcpyAsync(*dst, x, bytes, cudaMemcpyDefault, stream);
+    if (e != cudaSuccess) {
+        cudaFreeAsync(*dst, stream);
+        *dst = nullptr;
+    }
+    return e;
+}
+
+cudaError_t launch_segment(const Segment &seg, const ScoreArgs &args0, int device,
                            cudaStream_t stream) {
-    if (args.n <= 0) return cudaSuccess;
+    if (args0.n <= 0) return cudaSuccess;
+    if (args0.x_mapped && seg.layout != kSplit) {
+        // the irregular and L1-path kernels may read a row more than once
+        // (tree splits, per-visit global loads): score from a device copy
+        float *xd = nullptr;
+        cudaError_t e = x_device_copy(args0.x, args0.n, args0.ld, device, stream, &xd);
+        if (e != cudaSuccess) return e;
+        ScoreArgs a2 = args0;
+        a2.x_mapped = 0;
+        if (xd) a2.x = xd;
+        e = launch_segment(seg, a2, device, stream);
+        if (xd) {
+            const cudaError_t f = cudaFreeAsync(xd, stream);
+            if (e == cudaSuccess) e = f;
+        }
+        return e;
+    }
+    const ScoreArgs &args = args0;
     if (seg.layout == kCStream) {
         CStreamArgs ca{};
         // the records encode x-tile offsets for the tile planned at pack time
@@ -313,6 +349,7 @@ cudaError_t launch_segment(const Segment &seg, const ScoreArgs &args, int device
             sa.ld_ord = args.ld_ord;
             sa.status = args.status;
             sa.pipe = args.pipe;
+            sa.x_mapped = args.x_mapped;
             return launch_stream(seg.depth, sa, device, stream);
         }
         return cudaErrorInvalidConfiguration;  // packed for a device it does not fit

@@ -291,6 +291,16 @@ cudaError_t launch_stream(int D, const StreamArgs &a0, int device, cudaStream_t 
         return stream_detail::kStreamTable[D](a, device, stream);
     }
     StreamArgs w = a;
+    float *xcopy = nullptr;
+    if (a.x_mapped) {
+        // every split CTA of a tile re-reads its rows: not over PCIe
+        e = x_device_copy(a.x, a.n, a.ld, device, stream, &xcopy);
+        if (e != cudaSuccess) {
+            cudaFreeAsync(scratch, stream);
+            return e;
+        }
+        if (xcopy) w.x = xcopy;
+    }
     w.splits = splits;
     w.leaf_out = scratch;
     w.leaf_T = T;
@@ -302,7 +312,11 @@ cudaError_t launch_stream(int D, const StreamArgs &a0, int device, cudaStream_t 
         count_launch();
         e = cudaGetLastError();
     }
-    const cudaError_t f = cudaFreeAsync(scratch, stream);
+    cudaError_t f = cudaFreeAsync(scratch, stream);
+    if (xcopy) {
+        const cudaError_t g = cudaFreeAsync(xcopy, stream);
+        if (f == cudaSuccess) f = g;
+    }
     return e != cudaSuccess ? e : f;
 }
 

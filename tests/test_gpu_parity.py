@@ -853,3 +853,39 @@ def test_concurrent_host_pipelines_overlap():
     for t in ts_:
         t.join()
     assert errors == []
+
+
+@pytest.mark.parametrize("n", [1, 2, 31, 120, 1927, 1928, 5000])
+def test_host_direct_path_boundary(n):
+    """Host batches up to 1 MB of rows take the zero-copy path (mapped pinned
+    rows read by the kernel, scores written back over PCIe, ts_capi.cpp
+    score_host_direct); larger ones the chunked copy pipeline.  Both sides of
+    the boundary (F=136: 1927 / 1928 rows) bit-exact, mixed-depth model (two
+    segments: the second accumulates into the mapped output), non-finite
+    input still raises."""
+    from paper_1212_2287_b200.synth import complete_flat
+    from paper_1212_2287_b200.model import FlatModel
+    rng = np.random.default_rng(n)
+    F = 136
+    parts = []
+    for d, T in ((4, 30), (7, 20)):
+        n_int = (1 << d) - 1
+        parts.append(complete_flat(F, d, rng.integers(0, F, (T, n_int)), rng.random((T, n_int)),
+                                   rng.standard_normal((T, 1 << d))))
+    a, b = parts
+    off = np.concatenate([a.tree_off[:-1], b.tree_off + a.tree_off[-1]])
+    flat = FlatModel(F, off, np.concatenate([a.weight, b.weight]), np.concatenate([a.fid, b.fid]),
+                     np.concatenate([a.value, b.value]), np.concatenate([a.left, b.left]),
+                     np.concatenate([a.right, b.right]))
+    ev = _ev(flat)
+    x = rng.random((n, F), dtype=np.float32)
+    ref = oracle.COracle(flat.arrays()).score(x)
+    for _ in range(3):
+        assert np.array_equal(ev.predict_batch(x), ref)
+    if n <= 121:
+        assert ev.predict(x[0]) == ref[0]
+    x[n // 2, 7] = np.inf
+    with pytest.raises(ValueError):
+        ev.predict_batch(x)
+    x[n // 2, 7] = 0.5
+    assert np.array_equal(ev.predict_batch(x), oracle.COracle(flat.arrays()).score(x))
