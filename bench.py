@@ -30,8 +30,13 @@ may share a GPU -- a flow check, not a scaling number).  NCCL_DEBUG=INFO
 stays on for N > 1 so rank counts show in the log.
 
 ``--impl reference`` times the reference algorithm's CPU implementation on
-the host cores (the C restatement in oracle/, all threads, VPred lockstep
-batches) on a bounded row sample of the same workload; rank 0 only.
+the host cores on a bounded row sample of the same workload, rank 0 only:
+the faster of its two CPU strategies -- the VPred path
+(the C restatement in oracle/, all threads, lockstep batches of 64) and its
+CodeGen strategy (the reference's own generated C, byte-identical emitter in
+oracle/codegen.py, prebuilt by ``__graft_entry__.build``, one thread per
+core).  On the B200 hosts VPred is 4-16x faster (profiles/r2_cpu_baselines.jsonl),
+so it is the arm; both rates ride in ``cpu_baseline.candidates``.
 """
 
 from __future__ import annotations
