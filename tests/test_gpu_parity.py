@@ -889,3 +889,26 @@ def test_host_direct_path_boundary(n):
         ev.predict_batch(x)
     x[n // 2, 7] = 0.5
     assert np.array_equal(ev.predict_batch(x), oracle.COracle(flat.arrays()).score(x))
+
+
+@pytest.mark.parametrize("depth", [11, 12])
+@pytest.mark.parametrize("F", [40, 300])
+def test_deep_levels_fid_widths(depth, F):
+    """Global-leaf depths (>= 11: node parts streamed, leaves read from L2)
+    with 1- and 2-byte deep fids (F > 256): scores and every per-tree ordinal
+    bit-exact, with exact ties (integer-valued features and thresholds)."""
+    import torch
+    from paper_1212_2287_b200.synth import complete_flat
+    rng = np.random.default_rng(depth * 1000 + F)
+    T, n = 24, 3000
+    n_int = (1 << depth) - 1
+    flat = complete_flat(F, depth, rng.integers(0, F, (T, n_int)),
+                         rng.integers(0, 8, (T, n_int)).astype(np.float32),
+                         rng.standard_normal((T, 1 << depth)))
+    X = rng.integers(0, 8, (n, F)).astype(np.float32)
+    s, o = oracle.COracle(flat.arrays()).score(X, threads=4, with_ordinals=True)
+    ev = _ev(flat)
+    assert np.array_equal(ev.predict_batch(X), s)
+    assert np.array_equal(ev.leaf_indices(X), o.astype(np.int64))
+    xd = torch.from_numpy(X).cuda()
+    assert np.array_equal(ev.score_device(xd).cpu().numpy(), s)
