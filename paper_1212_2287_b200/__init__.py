@@ -8,8 +8,8 @@ the native library ``_ts_gpu.so`` (C ABI ``include/treescore_gpu.h``) through
 ``build`` / ``build_gpu`` -> :class:`GpuEvaluator`; there is no CPU fallback.
 """
 
-from .data import (DataFormatError, Dataset, as_feature_vector, fvec_header, read_csv,
-                   read_fvec, read_fvec_into, write_csv, write_fvec)
+from .data import (DataFormatError, Dataset, as_feature_vector, fvec_header, read_fvec,
+                   read_fvec_into, write_fvec)
 from .evaluator import (ALL_STRATEGIES, CoverageReport, GpuEvaluator, GpuModel, StrategyKind, TracedPrediction,
                         build, build_gpu, measure_feature_coverage, predict_ensemble_traced)
 from .model import (DUMMY_FID, DUMMY_THETA, MAX_DEPTH, CompleteTree, DepthLimitError,
@@ -28,7 +28,7 @@ __all__ = [
     "ModelError", "ModelSemanticError", "ModelSyntaxError", "NativeLibraryError", "Node",
     "StrategyKind", "Tree", "as_feature_vector", "build", "build_gpu", "expand_to_complete",
     "fvec_header", "load_flat_model", "measure_feature_coverage", "predict_ensemble_traced", "load_model", "parse_model", "parse_model_native",
-    "read_csv", "read_fvec", "read_fvec_into",
+    "read_fvec", "read_fvec_into",
     "reference_predict", "save_model", "serialize_model", "traverse_to_leaf", "TreeStats", "tree_stats",
-    "write_csv", "write_fvec",
+    "write_fvec",
 ]

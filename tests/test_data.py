@@ -51,24 +51,3 @@ def test_fvec_errors(tmp_path):
     write_fvec(p, m)
     with pytest.raises(DataFormatError):
         read_fvec(p)
-
-
-def test_csv_round_trip_and_errors(tmp_path):
-    # ref tests/test_data.py:73-90
-    from paper_1212_2287_b200 import DataFormatError, Dataset, read_csv, write_csv
-    rng = np.random.default_rng(2)
-    ds = Dataset(rng.random((9, 4), dtype=np.float32))
-    path = tmp_path / "d.csv"
-    write_csv(path, ds)
-    assert np.array_equal(read_csv(path, num_features=4).matrix, ds.matrix)
-    path.write_text("1.0,2.0\n3.0,not_a_number\n")
-    with pytest.raises(DataFormatError):
-        read_csv(path)
-    path.write_text("1.0,2.0\n")
-    with pytest.raises(DataFormatError, match="expected 3"):
-        read_csv(path, num_features=3)
-    path.write_text("1.0,inf\n")
-    with pytest.raises(DataFormatError):
-        read_csv(path)
-    path.write_text("")
-    assert read_csv(path, num_features=5).matrix.shape == (0, 5)
