@@ -55,6 +55,37 @@ __global__ void __launch_bounds__(B, 2) walk(float *out, int salt, const __grid_
                     j[k] = 3u + (c0 ? 2u : 0u) + (c1 ? 1u : 0u);
                 }
                 l0 = 2;
+            } else if (MODE == 3) {
+                // levels 0-1 from the parameter bank, chains in two halves so
+                // at most 4 chains' records are live in uniform registers
+#pragma unroll
+                for (int h = 0; h < 2; h++) {
+#pragma unroll
+                    for (int k = h * (K / 2); k < (h + 1) * (K / 2); k++) {
+                        const uint2 r0 = top.rec[3 * (t + k)];
+                        float v;
+                        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(r0.x + xr));
+                        const bool c0 = v >= __uint_as_float(r0.y);
+                        const uint2 a1 = top.rec[3 * (t + k) + 1], a2 = top.rec[3 * (t + k) + 2];
+                        const uint32_t fx = c0 ? a2.x : a1.x, th = c0 ? a2.y : a1.y;
+                        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(fx + xr));
+                        const bool c1 = v >= __uint_as_float(th);
+                        j[k] = 3u + (c0 ? 2u : 0u) + (c1 ? 1u : 0u);
+                    }
+                    asm volatile("" ::: "memory");
+                }
+                l0 = 2;
+            } else if (MODE == 2) {
+                // level 0 only from the parameter bank (one record per chain
+                // live in uniform registers), levels 1..7 from shared memory
+#pragma unroll
+                for (int k = 0; k < K; k++) {
+                    const uint2 r0 = top.rec[3 * (t + k)];
+                    float v;
+                    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(r0.x + xr));
+                    j[k] = v >= __uint_as_float(r0.y) ? 2u : 1u;
+                }
+                l0 = 1;
             } else {
 #pragma unroll
                 for (int k = 0; k < K; k++) j[k] = 0;
@@ -114,7 +145,11 @@ int main() {
         top.rec[i] = make_uint2((uint32_t)(((i * 29) % F) * B * 4), 0x3f000000u);
     run<0>("smem", sms, mhz, top);
     run<1>("param", sms, mhz, top);
+    run<2>("param-l0", sms, mhz, top);
+    run<3>("param-h", sms, mhz, top);
     run<0>("smem", sms, mhz, top);
     run<1>("param", sms, mhz, top);
+    run<2>("param-l0", sms, mhz, top);
+    run<3>("param-h", sms, mhz, top);
     return 0;
 }
