@@ -54,6 +54,9 @@ def test_bench_one_gpu_line_and_reference_config():
     assert res.returncode == 0, res.stderr[-4000:]
     ours = _json_line(res.stdout)
     assert ours["n_gpus"] == 1 and ours["parity"]["bit_exact_vs_oracle"]
+    # both CPU strategies timed, the faster one reported
+    cand = ours["cpu_baseline"]["candidates"]
+    assert cand["port"] > 0 and "generated" in cand
     assert ours["cfg4a"]["parity"]["bit_exact_vs_oracle"]
     assert ours["cfg4b"]["parity"]["bit_exact_vs_oracle"]
     ref = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
