@@ -88,6 +88,8 @@ typedef struct {
     int32_t compact_trees;         /* trees packed in the child-index form   */
     int32_t device;
     int32_t unit_weights;          /* all weights == 1.0 */
+    int32_t rank_trees;            /* complete trees in the rank layout      */
+    int32_t reserved;
 } ts_model_info;
 
 /* Validate, pack and upload a model to `device`.  The description is only
@@ -104,6 +106,11 @@ int ts_pack(const ts_model_desc *desc, int device, ts_model **out);
  * TS_ERR_DEPTH, since no complete table exists for them. */
 #define TS_PACK_TRACE 1
 #define TS_PACK_ANY_DEPTH 2
+/* TS_PACK_NO_RANK keeps complete trees in the fp32-threshold layout instead
+ * of the rank layout deep trees otherwise get (thresholds replaced by their
+ * rank among the ensemble's distinct thresholds of the feature, instances
+ * ranked by a pre-pass; same results bit for bit).  ts_score_pipe needs it. */
+#define TS_PACK_NO_RANK 4
 #define TS_MAX_LINKED_DEPTH 31
 int ts_pack_ex(const ts_model_desc *desc, int device, int flags, ts_model **out);
 

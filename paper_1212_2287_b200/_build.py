@@ -18,7 +18,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 SO = os.environ.get("TS_GPU_SO") or os.path.join(HERE, "_ts_gpu.so")
 SOURCES = ["ts_kernels.cu", "ts_stream.cu", "ts_stream_i0.cu", "ts_stream_i1.cu",
-           "ts_stream_i2.cu", "ts_stream_i3.cu", "ts_stream_i4.cu", "ts_cstream.cu", "ts_cstream_w8.cu", "ts_cstream_w16.cu", "ts_trace.cu", "ts_synth.cu",
+           "ts_stream_i2.cu", "ts_stream_i3.cu", "ts_stream_i4.cu", "ts_cstream.cu", "ts_cstream_w8.cu", "ts_cstream_w16.cu", "ts_trace.cu", "ts_synth.cu", "ts_rank.cu", "ts_rank_i0.cu", "ts_rank_i1.cu", "ts_rank_i2.cu",
            "ts_pack.cpp", "ts_parse.cpp", "ts_capi.cpp", "ts_nccl.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -26,6 +26,7 @@ TS_ERR_UNSUPPORTED = 7
 TS_ERR_SYNTAX = 8
 TS_PACK_TRACE = 1
 TS_PACK_ANY_DEPTH = 2
+TS_PACK_NO_RANK = 4
 
 # Every symbol include/treescore_gpu.h declares (checked by the CPU tests).
 EXPORTS = ("ts_pack", "ts_pack_ex", "ts_trace", "ts_model_get_info", "ts_score", "ts_score_ex", "ts_score_host", "ts_free",
@@ -83,7 +84,9 @@ class ModelInfo(ctypes.Structure):
                 ("complete_trees", ctypes.c_int32),
                 ("compact_trees", ctypes.c_int32),
                 ("device", ctypes.c_int32),
-                ("unit_weights", ctypes.c_int32)]
+                ("unit_weights", ctypes.c_int32),
+                ("rank_trees", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
 
     def as_dict(self):
         return {name: getattr(self, name) for name, _ in self._fields_}

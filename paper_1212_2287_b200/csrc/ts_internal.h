@@ -36,7 +36,15 @@ namespace ts {
 //             instance tile (so 4 B fid is the feature's byte offset in the x
 //             tile, < 2^18); leaf {(4 B F) << 14 | self, value}; trees of
 //             <= 8191 nodes, grouped into chunks of <= kCStreamMaxT trees.
-enum Layout : int { kComplete = 0, kCompact = 1, kSplit = 2, kCStream = 3 };
+//  kRank:     a complete tree for the rank kernels (ts_rank.cu): every
+//             threshold replaced by its rank among the ensemble's distinct
+//             thresholds of the same feature, so a node is ONE 4-byte record
+//             rec = fid << 24 | rank (rank 1-based, < 2^15; kRankInf for
+//             dummy +inf nodes) in heap order, then 2^d fp32 leaves; the
+//             instances go through the same map (ts_rank.cu k_rank: rank(x) =
+//             number of distinct thresholds <= x), and x >= theta <=>
+//             rank(x) >= rank(theta) exactly.
+enum Layout : int { kComplete = 0, kCompact = 1, kSplit = 2, kCStream = 3, kRank = 4 };
 
 struct Segment {
     int layout;   // Layout
@@ -71,6 +79,19 @@ struct DeviceTables {
     // TS_PACK_TRACE only
     TraceNode *trace_nodes = nullptr;
     uint32_t *trace_base = nullptr;  // [T] first node of tree t
+    // kRank: per feature the sorted distinct thresholds (-0.0 folded into
+    // +0.0) of the rank-layout trees (the node ranks index them at pack time).
+    // The pre-pass searches each list as a complete binary search tree in
+    // breadth-first (Eytzinger) order padded with +inf to 2^L - 1 entries:
+    // rank = (leaf reached after L steps) - (2^L - 1), the same heap walk as
+    // the trees', and bank-conflict-light (a sorted array's binary search
+    // probes one bank from every lane); feature f's tree is
+    // rank_e[rank_eoff[f] .. rank_eoff[f + 1]).
+    float *rank_e = nullptr;
+    uint32_t *rank_eoff = nullptr;         // [F + 1]
+    int2 *rank_groups = nullptr;           // pre-pass feature groups {f0, f1}
+    int rank_ngroups = 0;
+    uint32_t rank_group_words = 0;         // largest group's float count (+ alignment)
 };
 
 // kComplete records store fid << kFidShift: the byte offset of feature fid's
@@ -114,6 +135,23 @@ inline SplitGeom split_geom(int d, int fw) {
 __host__ __device__
 #endif
 constexpr bool split_header(int d, int fw) { return fw == 1 && d >= 2 && d != 8; }
+// kRank record geometry: 4-byte records in heap order, then the leaves.
+constexpr uint32_t kRankInf = 0x7fffu;   // rank of a dummy (+inf) threshold
+constexpr int kRankMaxU = 0x7ffe;        // distinct thresholds per feature
+constexpr int kRankB = 256;              // rows per rank tile (R layout and kernel)
+struct RankGeom {
+    uint32_t leaf0, bytes;
+};
+inline RankGeom rank_geom(int d) {
+    RankGeom g;
+    g.leaf0 = ((((1u << d) - 1u) * 4u) + 15u) & ~15u;
+    g.bytes = (g.leaf0 + (1u << d) * 4u + 15u) & ~15u;
+    return g;
+}
+inline uint32_t rank_ring_bytes(int d) {
+    const RankGeom g = rank_geom(d);
+    return d >= 11 ? g.leaf0 : g.bytes;  // node part only at global-leaf depths
+}
 // Bytes of one tree in a ring stage: the node part for global-leaf depths.
 inline uint32_t split_ring_bytes(int d, int fw) {
     const SplitGeom g = split_geom(d, fw);
@@ -273,6 +311,12 @@ struct CStreamArgs {
     int32_t *status;
 };
 bool plan_cstream(int F, int device, CStreamArgs *a);
+
+// Rank kernels (ts_rank.cu): whether depth D over F features has a plan on
+// this device, and the launch of one kRank segment (pre-pass + walk).
+bool rank_plan_ok(int F, int D, int device);
+cudaError_t launch_rank_segment(const Segment &seg, const ScoreArgs &args, int device,
+                                cudaStream_t stream);
 cudaError_t launch_cstream(const CStreamArgs &a, int device, cudaStream_t stream);
 
 // Launch the kernel of one segment; returns cudaSuccess or the launch error.

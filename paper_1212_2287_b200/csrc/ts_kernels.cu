@@ -290,6 +290,7 @@ cudaError_t x_device_copy(const float *x, long long n, long long ld, int device,
 cudaError_t launch_segment(const Segment &seg, const ScoreArgs &args0, int device,
                            cudaStream_t stream) {
     if (args0.n <= 0) return cudaSuccess;
+    if (seg.layout == kRank) return launch_rank_segment(seg, args0, device, stream);
     if (args0.x_mapped && seg.layout != kSplit) {
         // the irregular and L1-path kernels may read a row more than once
         // (tree splits, per-visit global loads): score from a device copy

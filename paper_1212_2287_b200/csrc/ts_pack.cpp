@@ -11,6 +11,7 @@
 #include <math.h>
 #include <string.h>
 
+#include <cmath>
 #include <algorithm>
 #include <cstdlib>
 #include <cstdio>
@@ -175,6 +176,28 @@ void fill_split(const int32_t *fid, const float *val, const int32_t *lc, const i
     memcpy(out + g.leaf0, hl.data(), hl.size() * 4);
 }
 
+// kRank: 4-byte records fid << 24 | rank (see Layout), then the leaves.
+// u: the feature's sorted distinct thresholds (rank = 1-based position).
+void fill_rank(const int32_t *fid, const float *val, const int32_t *lc, const int32_t *rc,
+               int depth, const std::vector<float> &u, const std::vector<uint32_t> &uoff,
+               unsigned char *out) {
+    std::vector<uint32_t> hf;
+    std::vector<float> ht, hl;
+    expand_heap(fid, val, lc, rc, depth, &hf, &ht, &hl);
+    const RankGeom g = rank_geom(depth);
+    uint32_t *recs = reinterpret_cast<uint32_t *>(out);
+    for (size_t j = 0; j < hf.size(); j++) {
+        uint32_t rank = kRankInf;  // dummy padding node (+inf): never taken
+        if (!(std::isinf(ht[j]) && ht[j] > 0)) {
+            const float th = ht[j] == 0.0f ? 0.0f : ht[j];  // -0.0 is +0.0 here
+            const float *b = u.data() + uoff[hf[j]], *e = u.data() + uoff[hf[j] + 1];
+            rank = (uint32_t)(std::upper_bound(b, e, th) - b);  // its own 1-based position
+        }
+        recs[j] = hf[j] << 24 | rank;
+    }
+    memcpy(out + g.leaf0, hl.data(), hl.size() * 4);
+}
+
 // Compact BFS layout with adjacent sibling pairs and self-loop leaves.
 // xstride 0: kCompact {fid | left << 16, theta}; xstride 4B: kCStream
 // {(xstride * fid) << 14 | left, theta} (ts_internal.h).
@@ -228,6 +251,9 @@ void free_tables(DeviceTables *t) {
     cudaFree(t->trace_base);
     cudaFree(t->chunk_info);
     cudaFree(t->slot_meta);
+    cudaFree(t->rank_e);
+    cudaFree(t->rank_eoff);
+    cudaFree(t->rank_groups);
     *t = DeviceTables{};
 }
 
@@ -308,9 +334,62 @@ extern "C" int ts_pack_ex(const ts_model_desc *d, int device, int flags, ts_mode
         max_depth = std::max(max_depth, s.depth);
     }
     // Blob layout: tree t at 16 * tree_off16[t] (see DeviceTables).
+    // Rank layout for the streamable complete trees of depth >= TS_RANK_MIN_DEPTH
+    // (default 12): when every feature has <= kRankMaxU distinct thresholds
+    // among them.  Deep trees are shared-memory-capacity-bound; 4-byte
+    // records and 2-byte instance ranks give them twice the lockstep chains,
+    // but the instance-rank pre-pass costs ~1.4 ms per 1M x 136 rows, so it
+    // pays only at d = 12 (10.3 -> 8.2 ms; d <= 11 slower:
+    // profiles/r2_rank_layout.txt).  TS_RANK=0 or TS_PACK_NO_RANK keeps the
+    // fp32 layout.
+    std::vector<float> rank_u;
+    std::vector<uint32_t> rank_off;
+    {
+        const char *re = getenv("TS_RANK");
+        const char *rd = getenv("TS_RANK_MIN_DEPTH");
+        const int min_d = rd ? atoi(rd) : 12;
+        bool want = !(flags & TS_PACK_NO_RANK) && F <= 256 && !(re && atoi(re) == 0) &&
+                    kernel_path() == 0;
+        bool rank_ok[TS_MAX_DEPTH + 1] = {};
+        if (want && cudaSetDevice(device) == cudaSuccess) {
+            for (int dd = std::max(1, min_d); dd <= TS_MAX_DEPTH; dd++)
+                rank_ok[dd] = rank_plan_ok(F, dd, device);
+            if (prev_dev >= 0) cudaSetDevice(prev_dev);
+        }
+        std::vector<std::vector<float>> per(F);
+        bool any = false;
+        for (int t = 0; want && t < T; t++) {
+            if (layout[t] != kSplit || shapes[t].depth < min_d || !rank_ok[shapes[t].depth])
+                continue;
+            any = true;
+            const int64_t o = d->tree_node_offset[t], nn = d->tree_node_offset[t + 1] - o;
+            for (int64_t i = 0; i < nn; i++) {
+                const int32_t f = d->node_fid[o + i];
+                if (f < 0) continue;
+                const float v = d->node_value[o + i];
+                per[f].push_back(v == 0.0f ? 0.0f : v);
+            }
+        }
+        size_t maxu = 0;
+        for (int f = 0; any && f < F; f++) {
+            std::sort(per[f].begin(), per[f].end());
+            per[f].erase(std::unique(per[f].begin(), per[f].end()), per[f].end());
+            maxu = std::max(maxu, per[f].size());
+        }
+        if (any && maxu <= (size_t)kRankMaxU) {
+            rank_off.assign(F + 1, 0u);
+            for (int f = 0; f < F; f++) rank_off[f + 1] = rank_off[f] + (uint32_t)per[f].size();
+            rank_u.reserve(rank_off[F]);
+            for (int f = 0; f < F; f++) rank_u.insert(rank_u.end(), per[f].begin(), per[f].end());
+            for (int t = 0; t < T; t++)
+                if (layout[t] == kSplit && shapes[t].depth >= min_d && rank_ok[shapes[t].depth])
+                    layout[t] = kRank;
+        }
+    }
     std::vector<uint64_t> off(T + 1, 0);
     for (int t = 0; t < T; t++) {
         uint64_t bytes = layout[t] == kComplete ? complete_tree_bytes(shapes[t].depth)
+                         : layout[t] == kRank ? rank_geom(shapes[t].depth).bytes
                          : layout[t] == kSplit ? split_geom(shapes[t].depth, fw).bytes
                          : ((uint64_t)shapes[t].bfs.size() * 8u + 15u) & ~(uint64_t)15u;
         off[t + 1] = off[t] + bytes;
@@ -334,6 +413,8 @@ extern "C" int ts_pack_ex(const ts_model_desc *d, int device, int flags, ts_mode
             fill_complete(fid, val, lc, rcc, shapes[t].depth, dst);
         else if (layout[t] == kSplit)
             fill_split(fid, val, lc, rcc, shapes[t].depth, fw, dst);
+        else if (layout[t] == kRank)
+            fill_rank(fid, val, lc, rcc, shapes[t].depth, rank_u, rank_off, dst);
         else
             fill_compact(fid, val, lc, rcc, shapes[t], F, reinterpret_cast<uint2 *>(dst),
                          layout[t] == kCStream ? 4u * (uint32_t)cplan.B : 0u);
@@ -403,6 +484,53 @@ extern "C" int ts_pack_ex(const ts_model_desc *d, int device, int flags, ts_mode
     if (!rc) rc = upload(&m->dev.weight, weight);
     if (!rc) rc = upload(&m->dev.chunk_info, chunk_info);
     if (!rc) rc = upload(&m->dev.slot_meta, slot_meta);
+    if (!rc && !rank_off.empty()) {
+        // Eytzinger trees of the sorted lists (see DeviceTables), and the
+        // pre-pass's feature groups: consecutive features whose trees fit one
+        // CTA's shared memory together (<= 160 KB)
+        std::vector<uint32_t> eoff(F + 1, 0u);
+        for (int f = 0; f < F; f++) {
+            const uint32_t m_f = rank_off[f + 1] - rank_off[f];
+            uint32_t L = 0;
+            while (((1u << L) - 1u) < m_f) L++;
+            eoff[f + 1] = eoff[f] + ((1u << L) - 1u);
+        }
+        std::vector<float> et(eoff[F] + 4, INFINITY);
+        for (int f = 0; f < F; f++) {
+            const uint32_t n_f = eoff[f + 1] - eoff[f], m_f = rank_off[f + 1] - rank_off[f];
+            // in-order traversal of the complete BST = sorted order
+            uint32_t next = 0;
+            std::vector<uint32_t> stack;
+            uint32_t i = 0;
+            while (i < n_f || !stack.empty()) {
+                while (i < n_f) {
+                    stack.push_back(i);
+                    i = 2 * i + 1;
+                }
+                i = stack.back();
+                stack.pop_back();
+                et[eoff[f] + i] = next < m_f ? rank_u[rank_off[f] + next] : INFINITY;
+                next++;
+                i = 2 * i + 2;
+            }
+        }
+        std::vector<int2> groups;
+        constexpr uint32_t kMaxWords = 160 * 1024 / 4 - 8;
+        int f0 = 0;
+        uint32_t maxw = 0;
+        for (int f = 0; f <= F; f++) {
+            if (f == F || (f > f0 && eoff[f + 1] - eoff[f0] + 3 > kMaxWords)) {
+                groups.push_back(int2{f0, f});
+                maxw = std::max(maxw, eoff[f] - eoff[f0] + 4u);
+                f0 = f;
+            }
+        }
+        rc = upload(&m->dev.rank_e, et);
+        if (!rc) rc = upload(&m->dev.rank_eoff, eoff);
+        if (!rc) rc = upload(&m->dev.rank_groups, groups);
+        m->dev.rank_ngroups = (int)groups.size();
+        m->dev.rank_group_words = maxw;
+    }
     if (!rc && (flags & TS_PACK_TRACE)) {
         // logical trees for the tracer: file-order nodes, leaf ordinals left-to-right
         std::vector<TraceNode> tn(d->tree_node_offset[T]);
@@ -452,6 +580,7 @@ extern "C" int ts_pack_ex(const ts_model_desc *d, int device, int flags, ts_mode
     info.compact_trees = n_compact;
     info.device = device;
     info.unit_weights = unit ? 1 : 0;
+    info.rank_trees = (int32_t)std::count(layout.begin(), layout.end(), (int)kRank);
     *out = m;
     return TS_OK;
 }

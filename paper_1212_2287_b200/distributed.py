@@ -120,13 +120,14 @@ def plan(mode: str, n: int, flat: FlatModel, world: int, rank: int,
     raise ValueError(f"unknown shard mode {mode!r}")
 
 
-def gpu_scorer(flat: FlatModel, device: int):
+def gpu_scorer(flat: FlatModel, device: int, rank: bool = True):
     """Default per-rank scorer: the CUDA library on ``device``.
 
     Returns ``score(x, out, accumulate)`` over torch CUDA tensors.
+    ``rank=False`` packs the fp32 layout (the fused tree-p2p pipeline).
     """
     from .evaluator import GpuModel
-    model = GpuModel(flat, device)
+    model = GpuModel(flat, device, rank=rank)
 
     def score(x, out, accumulate=False):
         model.score(x, out=out, accumulate=accumulate)
@@ -167,7 +168,9 @@ class ShardedScorer:
         self.serialize = serialize
         self.plan = plan(mode, n_total, flat, self.world, self.rank, depths)
         shard = flat if mode == "instance" else flat.subset(*self.plan.trees)
-        self.score = (make_scorer or (lambda fm: gpu_scorer(fm, device)))(shard)
+        # the fused pipeline (tree-p2p) runs on the fp32 complete-tree layout
+        self.score = (make_scorer or (lambda fm: gpu_scorer(fm, device,
+                                                            rank=mode != "tree-p2p")))(shard)
         # gloo moves CPU tensors only: CUDA payloads are staged through the host
         self._stage = dist.get_backend(group) == "gloo"
         # tree-reduce on GPUs over NCCL goes through the C ABI's own reduction

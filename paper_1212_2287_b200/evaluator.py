@@ -88,7 +88,7 @@ class GpuModel:
     """Packed device tables of one ensemble on one GPU (``ts_pack``)."""
 
     def __init__(self, model, device: int | None = None, trace: bool = False,
-                 any_depth: bool = False):
+                 any_depth: bool = False, rank: bool = True):
         torch = _torch()
         if not torch.cuda.is_available():
             raise _lib.NativeLibraryError("no CUDA device: the GPU scorer has no CPU fallback")
@@ -106,7 +106,10 @@ class GpuModel:
         desc = _lib.ModelDesc(int(flat.num_features), int(flat.num_trees),
                               *[a.ctypes.data for a in arrs])
         handle = ctypes.c_void_p()
-        flags = (_lib.TS_PACK_TRACE if trace else 0) | (_lib.TS_PACK_ANY_DEPTH if any_depth else 0)
+        # rank=False keeps deep complete trees in the fp32 layout (the fused
+        # cross-GPU pipeline, score_pipe, runs on that layout only)
+        flags = ((_lib.TS_PACK_TRACE if trace else 0) | (_lib.TS_PACK_ANY_DEPTH if any_depth else 0)
+                 | (0 if rank else _lib.TS_PACK_NO_RANK))
         rc = lib.ts_pack_ex(ctypes.byref(desc), self.device, flags,
                             ctypes.byref(handle))
         if rc == _lib.TS_ERR_DEPTH:

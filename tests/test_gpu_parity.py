@@ -912,3 +912,79 @@ def test_deep_levels_fid_widths(depth, F):
     assert np.array_equal(ev.leaf_indices(X), o.astype(np.int64))
     xd = torch.from_numpy(X).cuda()
     assert np.array_equal(ev.score_device(xd).cpu().numpy(), s)
+
+
+def _rank_case(rng, depth, F, T, ties=False, weights=False):
+    """Complete trees with optional exact ties, -0.0 / +0.0 and subnormal
+    thresholds, and weights != 1."""
+    from paper_1212_2287_b200.synth import complete_flat
+    n_int = (1 << depth) - 1
+    fids = rng.integers(0, F, (T, n_int))
+    if ties:
+        thr = rng.integers(-3, 4, (T, n_int)).astype(np.float32)
+        thr[rng.random((T, n_int)) < 0.1] = np.float32(-0.0)
+    else:
+        thr = rng.random((T, n_int), dtype=np.float32)
+        thr[rng.random((T, n_int)) < 0.02] = np.float32(1e-40)   # subnormal
+    leaves = rng.standard_normal((T, 1 << depth))
+    w = rng.uniform(0.25, 2.0, T) if weights else None
+    return complete_flat(F, depth, fids, thr, leaves, weights=w)
+
+
+@pytest.mark.parametrize("depth", [1, 3, 6, 8, 11, 12])
+@pytest.mark.parametrize("ties", [False, True])
+def test_rank_layout_forced_all_depths(depth, ties, monkeypatch):
+    """The rank layout (ts_rank.cu: thresholds -> per-feature ranks, instances
+    ranked by the k_rank pre-pass, 4-byte records) forced at every depth with
+    TS_RANK_MIN_DEPTH=1: scores and every per-tree ordinal bit-exact against
+    the oracle, with exact ties, -0.0/+0.0 and subnormal thresholds, weights
+    != 1, ragged n, host and device inputs."""
+    import torch
+    monkeypatch.setenv("TS_RANK_MIN_DEPTH", "1")
+    rng = np.random.default_rng(31 * depth + ties)
+    F, T = 40, 37
+    flat = _rank_case(rng, depth, F, T, ties=ties, weights=True)
+    n = 1000 + 77 * depth
+    if ties:
+        X = rng.integers(-3, 4, (n, F)).astype(np.float32)
+        X[rng.random((n, F)) < 0.05] = np.float32(-0.0)
+    else:
+        X = rng.random((n, F), dtype=np.float32)
+        X[rng.random((n, F)) < 0.01] = np.float32(1e-40)
+    s, o = oracle.COracle(flat.arrays()).score(X, threads=4, with_ordinals=True)
+    ev = _ev(flat)
+    assert ev.model.info["rank_trees"] == T
+    assert np.array_equal(ev.predict_batch(X), s)
+    assert np.array_equal(ev.leaf_indices(X), o.astype(np.int64))
+    assert np.array_equal(ev.score_device(torch.from_numpy(X).cuda()).cpu().numpy(), s)
+
+
+def test_rank_layout_default_choice_and_opt_out(monkeypatch):
+    """By default only depth-12 trees take the rank layout (where it measured
+    faster); TS_RANK=0 and rank=False keep the fp32 layout; all three give
+    the same bits, and a non-finite input is still flagged on the rank path."""
+    from paper_1212_2287_b200 import GpuModel
+    from paper_1212_2287_b200.model import FlatModel
+    rng = np.random.default_rng(5)
+    F = 136
+    a = _rank_case(rng, 12, F, 6)
+    b = _rank_case(rng, 8, F, 9)
+    off = np.concatenate([a.tree_off[:-1], b.tree_off + a.tree_off[-1]])
+    flat = FlatModel(F, off, np.concatenate([a.weight, b.weight]), np.concatenate([a.fid, b.fid]),
+                     np.concatenate([a.value, b.value]), np.concatenate([a.left, b.left]),
+                     np.concatenate([a.right, b.right]))
+    X = rng.random((3000, F), dtype=np.float32)
+    ref = oracle.COracle(flat.arrays()).score(X, threads=4)
+    ev = _ev(flat)
+    assert ev.model.info["rank_trees"] == 6
+    assert np.array_equal(ev.predict_batch(X), ref)
+    assert GpuModel(flat, 0, rank=False).info["rank_trees"] == 0
+    monkeypatch.setenv("TS_RANK", "0")
+    ev0 = _ev(flat)
+    assert ev0.model.info["rank_trees"] == 0
+    assert np.array_equal(ev0.predict_batch(X), ref)
+    monkeypatch.delenv("TS_RANK")
+    X[1234, 77] = np.nan
+    with pytest.raises(ValueError):
+        ev.predict_batch(X)
+

@@ -36,7 +36,7 @@ def _run_sequential(flat, x, world, epochs=2):
     from paper_1212_2287_b200.distributed import tree_shards
     from paper_1212_2287_b200.evaluator import GpuModel, PipeBuffers
     shards = tree_shards(flat.depths(), world)
-    models = [GpuModel(flat.subset(a, b), 0) for a, b in shards]
+    models = [GpuModel(flat.subset(a, b), 0, rank=False) for a, b in shards]
     bufs = [None] + [PipeBuffers(x.shape[0], 0) for _ in range(world - 1)]
     xd = torch.from_numpy(x).cuda()
     outs = []
