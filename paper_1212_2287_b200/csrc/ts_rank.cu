@@ -169,10 +169,47 @@ bool rank_plan_ok(int F, int D, int device) {
 // walk (k_rstream), then the scratch goes back to the pool -- all
 // stream-ordered.  Mapped host rows are fine here: the pre-pass reads each
 // value once per feature group.
-cudaError_t launch_rank_segment(const Segment &seg, const ScoreArgs &args, int device,
+namespace {
+cudaError_t rank_chunk(const Segment &seg, const ScoreArgs &args, int device,
+                       cudaStream_t stream);
+}  // namespace
+
+// Rows go through in chunks of <= kRankChunkRows (the rank scratch stays
+// <= ~1.1 GB at F = 136); rows in mapped host memory (ts_score_host's small
+// batches) are first copied to the device -- the pre-pass reads every row
+// once per feature group, which over PCIe would cost far more than one copy.
+constexpr long long kRankChunkRows = 4ll << 20;
+cudaError_t launch_rank_segment(const Segment &seg, const ScoreArgs &args0, int device,
                                 cudaStream_t stream) {
+    if (args0.n <= 0) return cudaSuccess;
+    ScoreArgs args = args0;
+    float *xd = nullptr;
+    if (args.x_mapped) {
+        cudaError_t e = x_device_copy(args.x, args.n, args.ld, device, stream, &xd);
+        if (e != cudaSuccess) return e;
+        if (xd) args.x = xd;
+        args.x_mapped = 0;
+    }
+    cudaError_t e = cudaSuccess;
+    for (long long r0 = 0; r0 < args.n && e == cudaSuccess; r0 += kRankChunkRows) {
+        ScoreArgs c = args;
+        c.n = std::min(kRankChunkRows, args.n - r0);
+        c.x = args.x + r0 * args.ld;
+        c.out = args.out ? args.out + r0 : nullptr;
+        c.ord = args.ord ? args.ord + r0 : nullptr;  // row offset; ld_ord unchanged
+        e = rank_chunk(seg, c, device, stream);
+    }
+    if (xd) {
+        const cudaError_t f = cudaFreeAsync(xd, stream);
+        if (e == cudaSuccess) e = f;
+    }
+    return e;
+}
+
+namespace {
+cudaError_t rank_chunk(const Segment &seg, const ScoreArgs &args, int device,
+                       cudaStream_t stream) {
     using namespace rank_detail;
-    if (args.n <= 0) return cudaSuccess;
     const DeviceTables &tb = *args.tables;
     if (!tb.rank_e || tb.rank_ngroups < 1) return cudaErrorInvalidConfiguration;
     RankArgs a{};
@@ -227,5 +264,6 @@ cudaError_t launch_rank_segment(const Segment &seg, const ScoreArgs &args, int d
     const cudaError_t f = cudaFreeAsync(R, stream);
     return e != cudaSuccess ? e : f;
 }
+}  // namespace
 
 }  // namespace ts
