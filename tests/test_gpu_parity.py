@@ -965,6 +965,8 @@ def test_rank_layout_default_choice_and_opt_out(monkeypatch):
     the same bits, and a non-finite input is still flagged on the rank path."""
     from paper_1212_2287_b200 import GpuModel
     from paper_1212_2287_b200.model import FlatModel
+    monkeypatch.delenv("TS_RANK_MIN_DEPTH", raising=False)
+    monkeypatch.delenv("TS_RANK", raising=False)
     rng = np.random.default_rng(5)
     F = 136
     a = _rank_case(rng, 12, F, 6)
@@ -997,6 +999,8 @@ def test_rank_layout_segments_chunks_and_host_paths(monkeypatch):
     path (mapped rows copied to the device before the pre-pass): bit-exact."""
     import torch
     from paper_1212_2287_b200.model import FlatModel
+    monkeypatch.delenv("TS_RANK_MIN_DEPTH", raising=False)
+    monkeypatch.delenv("TS_RANK", raising=False)
     rng = np.random.default_rng(77)
     # a depth-6 fp32 segment then a depth-12 rank segment (default threshold)
     F = 50
