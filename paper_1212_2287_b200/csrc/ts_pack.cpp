@@ -495,7 +495,7 @@ extern "C" int ts_pack_ex(const ts_model_desc *d, int device, int flags, ts_mode
             while (((1u << L) - 1u) < m_f) L++;
             eoff[f + 1] = eoff[f] + ((1u << L) - 1u);
         }
-        std::vector<float> et(eoff[F] + 4, INFINITY);
+        std::vector<float> et(eoff[F] + 8, INFINITY);  // the pre-pass reads whole 16-byte granules
         for (int f = 0; f < F; f++) {
             const uint32_t n_f = eoff[f + 1] - eoff[f], m_f = rank_off[f + 1] - rank_off[f];
             // in-order traversal of the complete BST = sorted order
@@ -521,7 +521,7 @@ extern "C" int ts_pack_ex(const ts_model_desc *d, int device, int flags, ts_mode
         for (int f = 0; f <= F; f++) {
             if (f == F || (f > f0 && eoff[f + 1] - eoff[f0] + 3 > kMaxWords)) {
                 groups.push_back(int2{f0, f});
-                maxw = std::max(maxw, eoff[f] - eoff[f0] + 4u);
+                maxw = std::max(maxw, eoff[f] - eoff[f0] + 8u);  // + 16-byte alignment lead and tail
                 f0 = f;
             }
         }
