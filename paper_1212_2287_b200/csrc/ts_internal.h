@@ -139,6 +139,8 @@ constexpr bool split_header(int d, int fw) { return fw == 1 && d >= 2 && d != 8;
 constexpr uint32_t kRankInf = 0x7fffu;   // rank of a dummy (+inf) threshold
 constexpr int kRankMaxU = 0x7ffe;        // distinct thresholds per feature
 constexpr int kRankB = 256;              // rows per rank tile (R layout and kernel)
+constexpr int kRankMaxDepth = 14;        // deepest tree the rank walk streams (d = 13-14:
+                                         // the fp32 layouts only have the L1 path there)
 struct RankGeom {
     uint32_t leaf0, bytes;
 };

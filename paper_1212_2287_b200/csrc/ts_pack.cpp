@@ -334,33 +334,48 @@ extern "C" int ts_pack_ex(const ts_model_desc *d, int device, int flags, ts_mode
         max_depth = std::max(max_depth, s.depth);
     }
     // Blob layout: tree t at 16 * tree_off16[t] (see DeviceTables).
-    // Rank layout for the streamable complete trees of depth >= TS_RANK_MIN_DEPTH
-    // (default 12): when every feature has <= kRankMaxU distinct thresholds
-    // among them.  Deep trees are shared-memory-capacity-bound; 4-byte
-    // records and 2-byte instance ranks give them twice the lockstep chains,
-    // but the instance-rank pre-pass costs ~1.4 ms per 1M x 136 rows, so it
-    // pays only at d = 12 (10.3 -> 8.2 ms; d <= 11 slower:
-    // profiles/r2_rank_layout.txt).  TS_RANK=0 or TS_PACK_NO_RANK keeps the
-    // fp32 layout.
+    // Rank layout (ts_rank.cu) for complete trees where it measured faster:
+    // the instance-rank pre-pass costs ~1.4 ms per 1M rows x 136 features
+    // whatever the ensemble, the walk saves per tree -- a lot where the fp32
+    // layouts are capacity-starved (d = 12) or have only the L1 path (d =
+    // 13-14), little at d = 10-11, nothing below (profiles/r2_rank_layout.txt).
+    // So a depth takes the rank layout when it has at least kRankMinTrees[d] x
+    // F / 136 trees (the break-even, rounded up), and every feature has <=
+    // kRankMaxU distinct thresholds among them.  TS_RANK_MIN_DEPTH=d forces it
+    // for all depths >= d (tests); TS_RANK=0 or TS_PACK_NO_RANK never.
     std::vector<float> rank_u;
     std::vector<uint32_t> rank_off;
     {
         const char *re = getenv("TS_RANK");
         const char *rd = getenv("TS_RANK_MIN_DEPTH");
-        const int min_d = rd ? atoi(rd) : 12;
+        const int forced_d = rd ? atoi(rd) : -1;
         bool want = !(flags & TS_PACK_NO_RANK) && F <= 256 && !(re && atoi(re) == 0) &&
                     kernel_path() == 0;
         bool rank_ok[TS_MAX_DEPTH + 1] = {};
         if (want && cudaSetDevice(device) == cudaSuccess) {
-            for (int dd = std::max(1, min_d); dd <= TS_MAX_DEPTH; dd++)
-                rank_ok[dd] = rank_plan_ok(F, dd, device);
+            for (int dd = 1; dd <= kRankMaxDepth; dd++) rank_ok[dd] = rank_plan_ok(F, dd, device);
             if (prev_dev >= 0) cudaSetDevice(prev_dev);
         }
+        int count[TS_MAX_DEPTH + 1] = {};
+        for (int t = 0; want && t < T; t++)
+            if ((layout[t] == kSplit || layout[t] == kComplete) && rank_ok[shapes[t].depth])
+                count[shapes[t].depth]++;
+        static const int kRankMinTrees[kRankMaxDepth + 1] = {0, 0, 0, 0, 0, 0, 0, 0,
+                                                             0, 0, 2500, 2000, 500, 150, 300};
+        bool use_d[TS_MAX_DEPTH + 1] = {};
+        for (int dd = 1; dd <= kRankMaxDepth; dd++) {
+            if (!rank_ok[dd] || !count[dd]) continue;
+            if (forced_d >= 0) use_d[dd] = dd >= forced_d;
+            else use_d[dd] = kRankMinTrees[dd] > 0 &&
+                             (int64_t)count[dd] * 136 >= (int64_t)kRankMinTrees[dd] * F;
+        }
+        auto rank_tree = [&](int t) {
+            return (layout[t] == kSplit || layout[t] == kComplete) && use_d[shapes[t].depth];
+        };
         std::vector<std::vector<float>> per(F);
         bool any = false;
         for (int t = 0; want && t < T; t++) {
-            if (layout[t] != kSplit || shapes[t].depth < min_d || !rank_ok[shapes[t].depth])
-                continue;
+            if (!rank_tree(t)) continue;
             any = true;
             const int64_t o = d->tree_node_offset[t], nn = d->tree_node_offset[t + 1] - o;
             for (int64_t i = 0; i < nn; i++) {
@@ -382,8 +397,7 @@ extern "C" int ts_pack_ex(const ts_model_desc *d, int device, int flags, ts_mode
             rank_u.reserve(rank_off[F]);
             for (int f = 0; f < F; f++) rank_u.insert(rank_u.end(), per[f].begin(), per[f].end());
             for (int t = 0; t < T; t++)
-                if (layout[t] == kSplit && shapes[t].depth >= min_d && rank_ok[shapes[t].depth])
-                    layout[t] = kRank;
+                if (rank_tree(t)) layout[t] = kRank;
         }
     }
     std::vector<uint64_t> off(T + 1, 0);

@@ -17,14 +17,15 @@ namespace rank_detail {
     extern template cudaError_t launch_rank_d<D>(const RankArgs &, int, int, cudaStream_t);
 TS_RANK_EXTERN(1) TS_RANK_EXTERN(2) TS_RANK_EXTERN(3) TS_RANK_EXTERN(4) TS_RANK_EXTERN(5)
 TS_RANK_EXTERN(6) TS_RANK_EXTERN(7) TS_RANK_EXTERN(8) TS_RANK_EXTERN(9) TS_RANK_EXTERN(10)
-TS_RANK_EXTERN(11) TS_RANK_EXTERN(12)
+TS_RANK_EXTERN(11) TS_RANK_EXTERN(12) TS_RANK_EXTERN(13) TS_RANK_EXTERN(14)
 #undef TS_RANK_EXTERN
 
 using RankFn = cudaError_t (*)(const RankArgs &, int, int, cudaStream_t);
-const RankFn kRankTable[kStreamMaxDepth + 1] = {
+const RankFn kRankTable[kRankMaxDepth + 1] = {
     nullptr,           launch_rank_d<1>,  launch_rank_d<2>,  launch_rank_d<3>, launch_rank_d<4>,
     launch_rank_d<5>,  launch_rank_d<6>,  launch_rank_d<7>,  launch_rank_d<8>, launch_rank_d<9>,
-    launch_rank_d<10>, launch_rank_d<11>, launch_rank_d<12>};
+    launch_rank_d<10>, launch_rank_d<11>, launch_rank_d<12>, launch_rank_d<13>,
+    launch_rank_d<14>};
 
 // ---------------------------------------------------------------------------
 // Pre-pass: instance ranks.  Block (feature group g, slice s): the group's
@@ -124,7 +125,7 @@ __global__ void __launch_bounds__(256) k_rank(RankPrepArgs a) {
 // Shared-memory plan of the walk: the 256-row u16 rank tile plus a ring of
 // 2-4 stages of whole K-groups (the tuned K, else the fallback).
 bool plan_rank(int F, int D, int device, RankArgs *a, int *k) {
-    if (D < 1 || D > kStreamMaxDepth || F > 256) return false;
+    if (D < 1 || D > kRankMaxDepth || F > 256) return false;
     const int optin = dev_attrs(device).smem_optin;
     if (!optin) return false;
     const size_t xs = ((size_t)F * kRankB * 2 + 127) & ~(size_t)127;

@@ -253,10 +253,10 @@ namespace rank_detail {
 // Lockstep chains per depth: the tuned count, then a fallback for rows too
 // wide to leave two ring stages of the tuned K-group.
 __host__ __device__ constexpr int rank_chains(int d) {
-    return d <= 8 ? 8 : d <= 10 ? 8 : d == 11 ? 6 : 4;
+    return d <= 8 ? 8 : d <= 10 ? 8 : d == 11 ? 6 : d == 12 ? 4 : d == 13 ? 2 : 1;
 }
 __host__ __device__ constexpr int rank_chains_fallback(int d) {
-    return d <= 10 ? 4 : d == 11 ? 3 : 2;
+    return d <= 10 ? 4 : d == 11 ? 3 : d == 12 ? 2 : 1;
 }
 
 template <int D>

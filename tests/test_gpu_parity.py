@@ -931,7 +931,7 @@ def _rank_case(rng, depth, F, T, ties=False, weights=False):
     return complete_flat(F, depth, fids, thr, leaves, weights=w)
 
 
-@pytest.mark.parametrize("depth", [1, 3, 6, 8, 11, 12])
+@pytest.mark.parametrize("depth", [1, 3, 6, 8, 11, 12, 13, 14])
 @pytest.mark.parametrize("ties", [False, True])
 def test_rank_layout_forced_all_depths(depth, ties, monkeypatch):
     """The rank layout (ts_rank.cu: thresholds -> per-feature ranks, instances
@@ -960,25 +960,30 @@ def test_rank_layout_forced_all_depths(depth, ties, monkeypatch):
 
 
 def test_rank_layout_default_choice_and_opt_out(monkeypatch):
-    """By default only depth-12 trees take the rank layout (where it measured
-    faster); TS_RANK=0 and rank=False keep the fp32 layout; all three give
-    the same bits, and a non-finite input is still flagged on the rank path."""
+    """By default a depth takes the rank layout only with enough trees for
+    the walk's savings to pay for the instance-rank pre-pass (ts_pack.cpp
+    kRankMinTrees x F / 136: 150 at d = 13, 500 at d = 12, never below
+    d = 10): here the 50 depth-13 trees do (F = 40), the 6 depth-12 and 9
+    depth-8 trees do not.  TS_RANK=0 and rank=False keep the fp32 layout; all
+    give the same bits, and a non-finite input is still flagged."""
     from paper_1212_2287_b200 import GpuModel
     from paper_1212_2287_b200.model import FlatModel
     monkeypatch.delenv("TS_RANK_MIN_DEPTH", raising=False)
     monkeypatch.delenv("TS_RANK", raising=False)
     rng = np.random.default_rng(5)
-    F = 136
-    a = _rank_case(rng, 12, F, 6)
-    b = _rank_case(rng, 8, F, 9)
-    off = np.concatenate([a.tree_off[:-1], b.tree_off + a.tree_off[-1]])
-    flat = FlatModel(F, off, np.concatenate([a.weight, b.weight]), np.concatenate([a.fid, b.fid]),
-                     np.concatenate([a.value, b.value]), np.concatenate([a.left, b.left]),
-                     np.concatenate([a.right, b.right]))
+    F = 40
+    parts = [_rank_case(rng, 13, F, 50), _rank_case(rng, 12, F, 6), _rank_case(rng, 8, F, 9)]
+    offs, acc = [], 0
+    for p_ in parts:
+        offs.append(p_.tree_off[:-1] + acc)
+        acc += p_.tree_off[-1]
+    off = np.concatenate(offs + [np.array([acc])])
+    cat = lambda k: np.concatenate([getattr(p_, k) for p_ in parts])  # noqa: E731
+    flat = FlatModel(F, off, cat("weight"), cat("fid"), cat("value"), cat("left"), cat("right"))
     X = rng.random((3000, F), dtype=np.float32)
     ref = oracle.COracle(flat.arrays()).score(X, threads=4)
     ev = _ev(flat)
-    assert ev.model.info["rank_trees"] == 6
+    assert ev.model.info["rank_trees"] == 50
     assert np.array_equal(ev.predict_batch(X), ref)
     assert GpuModel(flat, 0, rank=False).info["rank_trees"] == 0
     monkeypatch.setenv("TS_RANK", "0")
@@ -986,10 +991,9 @@ def test_rank_layout_default_choice_and_opt_out(monkeypatch):
     assert ev0.model.info["rank_trees"] == 0
     assert np.array_equal(ev0.predict_batch(X), ref)
     monkeypatch.delenv("TS_RANK")
-    X[1234, 77] = np.nan
+    X[1234, 17] = np.nan
     with pytest.raises(ValueError):
         ev.predict_batch(X)
-
 
 
 def test_rank_layout_segments_chunks_and_host_paths(monkeypatch):
@@ -999,10 +1003,10 @@ def test_rank_layout_segments_chunks_and_host_paths(monkeypatch):
     path (mapped rows copied to the device before the pre-pass): bit-exact."""
     import torch
     from paper_1212_2287_b200.model import FlatModel
-    monkeypatch.delenv("TS_RANK_MIN_DEPTH", raising=False)
+    monkeypatch.setenv("TS_RANK_MIN_DEPTH", "12")
     monkeypatch.delenv("TS_RANK", raising=False)
     rng = np.random.default_rng(77)
-    # a depth-6 fp32 segment then a depth-12 rank segment (default threshold)
+    # a depth-6 fp32 segment then a depth-12 rank segment (forced from d = 12)
     F = 50
     a = _rank_case(rng, 6, F, 7, weights=True)
     b = _rank_case(rng, 12, F, 3, weights=True)
