@@ -67,7 +67,10 @@ cudaMemPool_t scratch_pool(int device) {
             pools[device] = nullptr;
             return;
         }
-        uint64_t keep = 512ull << 20;
+        // keep up to 2 GB cached between calls: large per-call scratch (the
+        // rank path's instance ranks, the small-batch tree split's terms)
+        // would otherwise be unmapped and remapped on every call
+        uint64_t keep = 2048ull << 20;
         cudaMemPoolSetAttribute(pools[device], cudaMemPoolAttrReleaseThreshold, &keep);
     });
     return pools[device];

@@ -176,10 +176,11 @@ cudaError_t rank_chunk(const Segment &seg, const ScoreArgs &args, int device,
 }  // namespace
 
 // Rows go through in chunks of <= kRankChunkRows (the rank scratch stays
-// <= ~1.1 GB at F = 136); rows in mapped host memory (ts_score_host's small
+// <= ~0.6 GB at F = 136, within what the pool keeps cached between calls);
+// rows in mapped host memory (ts_score_host's small
 // batches) are first copied to the device -- the pre-pass reads every row
 // once per feature group, which over PCIe would cost far more than one copy.
-constexpr long long kRankChunkRows = 4ll << 20;
+constexpr long long kRankChunkRows = 2ll << 20;
 cudaError_t launch_rank_segment(const Segment &seg, const ScoreArgs &args0, int device,
                                 cudaStream_t stream) {
     if (args0.n <= 0) return cudaSuccess;

@@ -998,7 +998,7 @@ def test_rank_layout_default_choice_and_opt_out(monkeypatch):
 
 def test_rank_layout_segments_chunks_and_host_paths(monkeypatch):
     """The rank path continuing a partial sum (a rank segment after an fp32
-    one), rows beyond one 4M-row rank chunk (ts_rank.cu kRankChunkRows: the
+    one), rows beyond one 2M-row rank chunk (ts_rank.cu kRankChunkRows: the
     ordinals' row offset, the sums' continuation), and the host small-batch
     path (mapped rows copied to the device before the pre-pass): bit-exact."""
     import torch
@@ -1023,14 +1023,14 @@ def test_rank_layout_segments_chunks_and_host_paths(monkeypatch):
         assert np.array_equal(ev.leaf_indices(X), o.astype(np.int64))
     # more rows than one rank chunk: small trees forced onto the rank layout
     monkeypatch.setenv("TS_RANK_MIN_DEPTH", "1")
-    F2, n2 = 4, (4 << 20) + 777
+    F2, n2 = 4, (2 << 20) + 777
     flat2 = _rank_case(rng, 3, F2, 5)
     ev2 = _ev(flat2)
     assert ev2.model.info["rank_trees"] == 5
     X2 = torch.rand((n2, F2), device="cuda")
     ords = torch.empty((5, n2), dtype=torch.int16, device="cuda")
     got = ev2.model.score(X2, ordinals=ords).cpu().numpy()
-    rows = np.concatenate([np.arange(0, 300), np.arange((4 << 20) - 300, n2)])
+    rows = np.concatenate([np.arange(0, 300), np.arange((2 << 20) - 300, n2)])
     xs = X2[torch.from_numpy(rows).cuda()].cpu().numpy()
     s2, o2 = oracle.COracle(flat2.arrays()).score(xs, threads=4, with_ordinals=True)
     assert np.array_equal(got[rows], s2)
