@@ -125,9 +125,10 @@ int ts_model_get_info(const ts_model *model, ts_model_info *info);
  *   stream   cudaStream_t (NULL = legacy default stream)
  * Stream-ordered; returns after enqueueing.  Allocates nothing from the
  * caller's heaps: small batches with long walks (the two-pass tree split)
- * take per-call scratch from the library's own stream-ordered memory pool
- * (cudaMallocFromPoolAsync / cudaFreeAsync on `stream`, so it stays
- * CUDA-graph capturable). */
+ * and rank-layout segments (deep complete trees: the instance ranks, 2 bytes
+ * per value, in chunks of <= 2M rows) take per-call scratch from the
+ * library's own stream-ordered memory pool (cudaMallocFromPoolAsync /
+ * cudaFreeAsync on `stream`, so it stays CUDA-graph capturable). */
 int ts_score(const ts_model *model, const float *x, int64_t n, int64_t f, int64_t ld,
              double *out, uint16_t *ord_out, int64_t ld_ord, int32_t *status,
              void *stream);
