@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(256) k_rank(RankPrepArgs a) {
 #pragma unroll
         for (int q = 0; q < kRows; q++) {
             if (tq + q < a.tiles) {
-                a.R[((tq + q) * a.F + f) * kRankB + r] = (uint16_t)(i[q] - nf);
+                a.R[((tq + q) * a.F + f) * kRankB + rank_slot((uint32_t)r)] = (uint16_t)(i[q] - nf);
                 bad |= (tq + q) * kRankB + r < a.n && !finite_f(v[q]);
             }
             v[q] = vn[q];

@@ -24,7 +24,8 @@
 //  * k_rstream<D, K>: k_stream's structure (persistent 256-row tiles, one
 //    producer warp streaming the segment's trees through a TMA ring, eight
 //    consumer warps walking K trees in lockstep) on kRank records:
-//        rec = LDS.32 [p];  v = LDS.U16 [xr + (rec >> 15)]   (= fid * 512)
+//        rec = LDS.32 [p];  v = LDS.U16 [xr + (rec >> 15)]   (= fid * 512;
+//                                                      xr: rank_slot(row))
 //        c = (v | rec & 0xff000000) >= rec                    (= rank(x) >= rank)
 //        p = 2p + (c ? 8 - base : 4 - base)                   (heap step)
 //    then w * leaf added in f64 in tree order (__dmul_rn / __dadd_rn).
@@ -36,6 +37,14 @@ namespace rank_detail {
 using namespace stream_detail;
 
 constexpr int kCW = 8;                  // consumer warps: 256-row tiles
+// u16 slot of row r (0..255) in a feature's 512-byte run of a rank tile:
+// warps 2k and 2k+1 share 32-bit words (low / high halves), lane l of a warp
+// in word 32k + l -- so a warp's 32 lanes read 32 distinct banks for any mix
+// of features (two rows of one warp in one word would be a 2-way conflict on
+// every x read).
+__host__ __device__ constexpr uint32_t rank_slot(uint32_t r) {
+    return ((((r >> 5) >> 1) << 5) + (r & 31u)) * 2u + ((r >> 5) & 1u);
+}
 constexpr int kThreads = kCW * 32 + 32;
 constexpr int kRankMaxStages = 4;
 
@@ -203,7 +212,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rstream(RankArgs a) {
 
     // ---- consumer warps
     const int r = threadIdx.x;
-    const uint32_t xr = su32(xs) + 2u * r;
+    const uint32_t xr = su32(xs) + 2u * rank_slot((uint32_t)r);
     const uint32_t TB = a.ring_tree_bytes;
     const int tile_vec = a.F * kB * 2 / 16;  // 16-byte pieces of a rank tile
     int s = 0;
