@@ -53,6 +53,7 @@ struct Segment {
     uint64_t byte0;  // blob offset of tree t0
     int chunk0 = 0, nchunks = 0;  // kCStream: chunk table range
     int cs_b = 0;                 // kCStream: instance tile the records were encoded for
+    int rank_space = 0;           // kRank: index into DeviceTables::rank_spaces
 };
 
 // All trees live in one byte blob, tree t at byte 16 * tree_off16[t]:
@@ -68,6 +69,24 @@ struct TraceNode {
     int32_t left, right;  // tree-local node ids
 };
 
+// A rank space: per feature the sorted distinct thresholds (-0.0 folded into
+// +0.0) of a run of rank-layout trees (their node ranks index these lists;
+// at most kRankMaxU per feature, so an ensemble with more distinct
+// thresholds is split into several spaces, each scored by its own
+// pre-pass).  The pre-pass searches each list as a complete binary search
+// tree in breadth-first (Eytzinger) order padded with +inf to 2^L - 1
+// entries: rank = (leaf reached after L steps) - (2^L - 1), the same heap
+// walk as the trees', and bank-conflict-light (a sorted array's binary
+// search probes one bank from every lane); feature f's tree is
+// e[eoff[f] .. eoff[f + 1]).
+struct RankSpace {
+    float *e = nullptr;
+    uint32_t *eoff = nullptr;        // [F + 1]
+    int2 *groups = nullptr;          // pre-pass feature groups {f0, f1}
+    int ngroups = 0;
+    uint32_t group_words = 0;        // largest group's float count (+ alignment)
+};
+
 struct DeviceTables {
     unsigned char *blob = nullptr;
     uint32_t *tree_off16 = nullptr;  // [T]
@@ -79,20 +98,11 @@ struct DeviceTables {
     // TS_PACK_TRACE only
     TraceNode *trace_nodes = nullptr;
     uint32_t *trace_base = nullptr;  // [T] first node of tree t
-    // kRank: per feature the sorted distinct thresholds (-0.0 folded into
-    // +0.0) of the rank-layout trees (the node ranks index them at pack time).
-    // The pre-pass searches each list as a complete binary search tree in
-    // breadth-first (Eytzinger) order padded with +inf to 2^L - 1 entries:
-    // rank = (leaf reached after L steps) - (2^L - 1), the same heap walk as
-    // the trees', and bank-conflict-light (a sorted array's binary search
-    // probes one bank from every lane); feature f's tree is
-    // rank_e[rank_eoff[f] .. rank_eoff[f + 1]).
-    float *rank_e = nullptr;
-    uint32_t *rank_eoff = nullptr;         // [F + 1]
-    int2 *rank_groups = nullptr;           // pre-pass feature groups {f0, f1}
-    int rank_ngroups = 0;
-    uint32_t rank_group_words = 0;         // largest group's float count (+ alignment)
+    // kRank: the rank spaces (RankSpace; a segment of kRank trees uses one)
+    std::vector<RankSpace> rank_spaces;
 };
+
+
 
 // kComplete records store fid << kFidShift: the byte offset of feature fid's
 // row in the streaming kernel's 256-instance x tile (256 * 4 = 1 << 10).

@@ -16,6 +16,7 @@
 #include <cstdlib>
 #include <cstdio>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "ts_internal.h"
@@ -251,9 +252,11 @@ void free_tables(DeviceTables *t) {
     cudaFree(t->trace_base);
     cudaFree(t->chunk_info);
     cudaFree(t->slot_meta);
-    cudaFree(t->rank_e);
-    cudaFree(t->rank_eoff);
-    cudaFree(t->rank_groups);
+    for (RankSpace &r : t->rank_spaces) {
+        cudaFree(r.e);
+        cudaFree(r.eoff);
+        cudaFree(r.groups);
+    }
     *t = DeviceTables{};
 }
 
@@ -343,8 +346,12 @@ extern "C" int ts_pack_ex(const ts_model_desc *d, int device, int flags, ts_mode
     // F / 136 trees (the break-even, rounded up), and every feature has <=
     // kRankMaxU distinct thresholds among them.  TS_RANK_MIN_DEPTH=d forces it
     // for all depths >= d (tests); TS_RANK=0 or TS_PACK_NO_RANK never.
-    std::vector<float> rank_u;
-    std::vector<uint32_t> rank_off;
+    struct RankHost {
+        std::vector<float> u;        // sorted distinct thresholds, feature-major
+        std::vector<uint32_t> off;   // [F + 1]
+    };
+    std::vector<RankHost> rank_hosts;
+    std::vector<int> space_of(T, -1);
     {
         const char *re = getenv("TS_RANK");
         const char *rd = getenv("TS_RANK_MIN_DEPTH");
@@ -372,33 +379,67 @@ extern "C" int ts_pack_ex(const ts_model_desc *d, int device, int flags, ts_mode
         auto rank_tree = [&](int t) {
             return (layout[t] == kSplit || layout[t] == kComplete) && use_d[shapes[t].depth];
         };
-        std::vector<std::vector<float>> per(F);
-        bool any = false;
+        // Rank spaces: consecutive runs of rank trees whose thresholds stay
+        // <= kRankMaxU per feature.  A space closes when the run's NODE count
+        // for some feature would pass the limit (an upper bound of its
+        // distinct thresholds, so no space overflows; repeated thresholds
+        // only make spaces smaller than they need be), then its lists are
+        // sorted and deduplicated once.
+        std::vector<std::vector<float>> per(F);   // the open space's values
+        std::vector<uint32_t> used(F, 0u);
+        auto close_space = [&]() {
+            RankHost h;
+            h.off.assign(F + 1, 0u);
+            {
+                auto su = [&](int f0, int f1) {
+                    for (int f = f0; f < f1; f++) {
+                        std::sort(per[f].begin(), per[f].end());
+                        per[f].erase(std::unique(per[f].begin(), per[f].end()), per[f].end());
+                    }
+                };
+                const int nth = (int)std::min<unsigned>(
+                    (unsigned)F, std::min(16u, std::max(1u, std::thread::hardware_concurrency())));
+                std::vector<std::thread> th;
+                for (int k = 0; k < nth; k++)
+                    th.emplace_back(su, F * k / nth, F * (k + 1) / nth);
+                for (auto &x : th) x.join();
+            }
+            for (int f = 0; f < F; f++) h.off[f + 1] = h.off[f] + (uint32_t)per[f].size();
+            h.u.reserve(h.off[F]);
+            for (int f = 0; f < F; f++) {
+                h.u.insert(h.u.end(), per[f].begin(), per[f].end());
+                per[f].clear();
+                used[f] = 0u;
+            }
+            rank_hosts.push_back(std::move(h));
+        };
+        std::vector<uint32_t> cnt(F);
+        bool open = false;
         for (int t = 0; want && t < T; t++) {
             if (!rank_tree(t)) continue;
-            any = true;
             const int64_t o = d->tree_node_offset[t], nn = d->tree_node_offset[t + 1] - o;
+            std::fill(cnt.begin(), cnt.end(), 0u);
+            for (int64_t i = 0; i < nn; i++)
+                if (d->node_fid[o + i] >= 0) cnt[d->node_fid[o + i]]++;
+            bool fits = true;
+            for (int f = 0; f < F && fits; f++) fits = used[f] + cnt[f] <= (uint32_t)kRankMaxU;
+            if (!fits && open) {
+                close_space();
+                open = false;
+            }
             for (int64_t i = 0; i < nn; i++) {
                 const int32_t f = d->node_fid[o + i];
                 if (f < 0) continue;
                 const float v = d->node_value[o + i];
                 per[f].push_back(v == 0.0f ? 0.0f : v);
             }
+            for (int f = 0; f < F; f++) used[f] += cnt[f];
+            space_of[t] = (int)rank_hosts.size();
+            open = true;
         }
-        size_t maxu = 0;
-        for (int f = 0; any && f < F; f++) {
-            std::sort(per[f].begin(), per[f].end());
-            per[f].erase(std::unique(per[f].begin(), per[f].end()), per[f].end());
-            maxu = std::max(maxu, per[f].size());
-        }
-        if (any && maxu <= (size_t)kRankMaxU) {
-            rank_off.assign(F + 1, 0u);
-            for (int f = 0; f < F; f++) rank_off[f + 1] = rank_off[f] + (uint32_t)per[f].size();
-            rank_u.reserve(rank_off[F]);
-            for (int f = 0; f < F; f++) rank_u.insert(rank_u.end(), per[f].begin(), per[f].end());
-            for (int t = 0; t < T; t++)
-                if (rank_tree(t)) layout[t] = kRank;
-        }
+        if (open) close_space();
+        for (int t = 0; t < T; t++)
+            if (space_of[t] >= 0) layout[t] = kRank;
     }
     std::vector<uint64_t> off(T + 1, 0);
     for (int t = 0; t < T; t++) {
@@ -414,24 +455,42 @@ extern "C" int ts_pack_ex(const ts_model_desc *d, int device, int flags, ts_mode
     std::vector<uint32_t> off16(T);
     std::vector<int32_t> depth(T);
     std::vector<double> weight(d->tree_weight, d->tree_weight + T);
-    for (int t = 0; t < T; t++) {
-        const int64_t o = d->tree_node_offset[t];
-        const int32_t *fid = d->node_fid + o;
-        const float *val = d->node_value + o;
-        const int32_t *lc = d->node_left + o;
-        const int32_t *rcc = d->node_right + o;
-        off16[t] = (uint32_t)(off[t] / 16);
-        depth[t] = shapes[t].depth;
-        unsigned char *dst = blob.data() + off[t];
-        if (layout[t] == kComplete)
-            fill_complete(fid, val, lc, rcc, shapes[t].depth, dst);
-        else if (layout[t] == kSplit)
-            fill_split(fid, val, lc, rcc, shapes[t].depth, fw, dst);
-        else if (layout[t] == kRank)
-            fill_rank(fid, val, lc, rcc, shapes[t].depth, rank_u, rank_off, dst);
-        else
-            fill_compact(fid, val, lc, rcc, shapes[t], F, reinterpret_cast<uint2 *>(dst),
-                         layout[t] == kCStream ? 4u * (uint32_t)cplan.B : 0u);
+    // Trees fill disjoint byte ranges of the blob: several host threads for
+    // big ensembles (config 4b: 20,000 depth-10 trees)
+    auto fill = [&](int t0, int t1) {
+        for (int t = t0; t < t1; t++) {
+            const int64_t o = d->tree_node_offset[t];
+            const int32_t *fid = d->node_fid + o;
+            const float *val = d->node_value + o;
+            const int32_t *lc = d->node_left + o;
+            const int32_t *rcc = d->node_right + o;
+            off16[t] = (uint32_t)(off[t] / 16);
+            depth[t] = shapes[t].depth;
+            unsigned char *dst = blob.data() + off[t];
+            if (layout[t] == kComplete)
+                fill_complete(fid, val, lc, rcc, shapes[t].depth, dst);
+            else if (layout[t] == kSplit)
+                fill_split(fid, val, lc, rcc, shapes[t].depth, fw, dst);
+            else if (layout[t] == kRank)
+                fill_rank(fid, val, lc, rcc, shapes[t].depth, rank_hosts[space_of[t]].u,
+                          rank_hosts[space_of[t]].off, dst);
+            else
+                fill_compact(fid, val, lc, rcc, shapes[t], F, reinterpret_cast<uint2 *>(dst),
+                             layout[t] == kCStream ? 4u * (uint32_t)cplan.B : 0u);
+        }
+    };
+    {
+        const int64_t nodes = d->tree_node_offset[T];
+        const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+        const int nth = nodes < (1 << 20) ? 1 : (int)std::min<unsigned>(16u, hw);
+        if (nth == 1) {
+            fill(0, T);
+        } else {
+            std::vector<std::thread> th;
+            for (int k = 0; k < nth; k++)
+                th.emplace_back(fill, (int)((int64_t)T * k / nth), (int)((int64_t)T * (k + 1) / nth));
+            for (auto &x : th) x.join();
+        }
     }
 
     ts_model *m = new ts_model();
@@ -442,15 +501,18 @@ extern "C" int ts_pack_ex(const ts_model_desc *d, int device, int flags, ts_mode
     for (int t = 0; t < T; t++) {
         const bool any_depth = layout[t] == kCompact || layout[t] == kCStream;
         const int key_depth = any_depth ? -1 : shapes[t].depth;
+        const int space = layout[t] == kRank ? space_of[t] : 0;
         if (!m->segments.empty()) {
             Segment &b = m->segments.back();
-            if (b.layout == layout[t] && (any_depth || b.depth == key_depth)) {
+            if (b.layout == layout[t] && (any_depth || b.depth == key_depth) &&
+                b.rank_space == space) {
                 b.t1 = t + 1;
                 continue;
             }
         }
         m->segments.push_back(Segment{layout[t], any_depth ? max_depth : key_depth, t, t + 1,
                                       off[t]});
+        m->segments.back().rank_space = space;
     }
     // kCStream chunk tables: consecutive trees up to tpc / chunk_cap bytes;
     // inside a chunk the slots are ordered by depth (deepest first) so the
@@ -498,10 +560,12 @@ extern "C" int ts_pack_ex(const ts_model_desc *d, int device, int flags, ts_mode
     if (!rc) rc = upload(&m->dev.weight, weight);
     if (!rc) rc = upload(&m->dev.chunk_info, chunk_info);
     if (!rc) rc = upload(&m->dev.slot_meta, slot_meta);
-    if (!rc && !rank_off.empty()) {
-        // Eytzinger trees of the sorted lists (see DeviceTables), and the
+    for (size_t sp = 0; !rc && sp < rank_hosts.size(); sp++) {
+        // Eytzinger trees of the space's sorted lists (see RankSpace), and the
         // pre-pass's feature groups: consecutive features whose trees fit one
         // CTA's shared memory together (<= 160 KB)
+        const std::vector<float> &rank_u = rank_hosts[sp].u;
+        const std::vector<uint32_t> &rank_off = rank_hosts[sp].off;
         std::vector<uint32_t> eoff(F + 1, 0u);
         for (int f = 0; f < F; f++) {
             const uint32_t m_f = rank_off[f + 1] - rank_off[f];
@@ -539,11 +603,13 @@ extern "C" int ts_pack_ex(const ts_model_desc *d, int device, int flags, ts_mode
                 f0 = f;
             }
         }
-        rc = upload(&m->dev.rank_e, et);
-        if (!rc) rc = upload(&m->dev.rank_eoff, eoff);
-        if (!rc) rc = upload(&m->dev.rank_groups, groups);
-        m->dev.rank_ngroups = (int)groups.size();
-        m->dev.rank_group_words = maxw;
+        m->dev.rank_spaces.emplace_back();
+        RankSpace &r = m->dev.rank_spaces.back();
+        rc = upload(&r.e, et);
+        if (!rc) rc = upload(&r.eoff, eoff);
+        if (!rc) rc = upload(&r.groups, groups);
+        r.ngroups = (int)groups.size();
+        r.group_words = maxw;
     }
     if (!rc && (flags & TS_PACK_TRACE)) {
         // logical trees for the tracer: file-order nodes, leaf ordinals left-to-right

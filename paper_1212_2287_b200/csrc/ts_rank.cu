@@ -29,7 +29,7 @@ const RankFn kRankTable[kRankMaxDepth + 1] = {
 
 // ---------------------------------------------------------------------------
 // Pre-pass: instance ranks.  Block (feature group g, slice s): the group's
-// Eytzinger trees rank_e[rank_eoff[f0] .. rank_eoff[f1]) are one contiguous
+// Eytzinger trees e[eoff[f0] .. eoff[f1]) (RankSpace) are one contiguous
 // run, loaded into shared memory once (bulk copies); then, for tiles s,
 // s + slices, ... kRows at a time, thread r ranks rows r, r + 256, ... for
 // every feature of the group: kRows independent L-step heap walks in flight
@@ -212,8 +212,11 @@ namespace {
 cudaError_t rank_chunk(const Segment &seg, const ScoreArgs &args, int device,
                        cudaStream_t stream) {
     using namespace rank_detail;
-    const DeviceTables &tb = *args.tables;
-    if (!tb.rank_e || tb.rank_ngroups < 1) return cudaErrorInvalidConfiguration;
+    const DeviceTables &dt = *args.tables;
+    if (seg.rank_space < 0 || (size_t)seg.rank_space >= dt.rank_spaces.size())
+        return cudaErrorInvalidConfiguration;
+    const RankSpace &tb = dt.rank_spaces[seg.rank_space];
+    if (!tb.e || tb.ngroups < 1) return cudaErrorInvalidConfiguration;
     RankArgs a{};
     int K = 0;
     if (!plan_rank(args.F, seg.depth, device, &a, &K)) return cudaErrorInvalidConfiguration;
@@ -230,20 +233,20 @@ cudaError_t rank_chunk(const Segment &seg, const ScoreArgs &args, int device,
         p.n = args.n;
         p.ld = args.ld;
         p.F = args.F;
-        p.e = tb.rank_e;
-        p.eoff = tb.rank_eoff;
-        p.groups = tb.rank_groups;
+        p.e = tb.e;
+        p.eoff = tb.eoff;
+        p.groups = tb.groups;
         p.R = R;
         p.status = args.status;
         p.tiles = tiles;
-        const size_t smem = std::max<size_t>(16, (size_t)tb.rank_group_words * 4);
+        const size_t smem = std::max<size_t>(16, (size_t)tb.group_words * 4);
         e = ensure_smem((const void *)k_rank, smem);
         if (e == cudaSuccess) {
             const int sms = dev_attrs(device).sms;
             const long long blocks = (tiles + kRows - 1) / kRows;
             const int slices = (int)std::max<long long>(
-                1, std::min<long long>(blocks, (2LL * sms + tb.rank_ngroups - 1) / tb.rank_ngroups));
-            k_rank<<<dim3((unsigned)tb.rank_ngroups, (unsigned)slices), 256, smem, stream>>>(p);
+                1, std::min<long long>(blocks, (2LL * sms + tb.ngroups - 1) / tb.ngroups));
+            k_rank<<<dim3((unsigned)tb.ngroups, (unsigned)slices), 256, smem, stream>>>(p);
             count_launch();
             e = cudaGetLastError();
         }

@@ -1035,3 +1035,24 @@ def test_rank_layout_segments_chunks_and_host_paths(monkeypatch):
     s2, o2 = oracle.COracle(flat2.arrays()).score(xs, threads=4, with_ordinals=True)
     assert np.array_equal(got[rows], s2)
     assert np.array_equal(ords.cpu().numpy().view(np.uint16)[:, rows], o2)
+
+
+def test_rank_layout_several_rank_spaces(monkeypatch):
+    """More distinct thresholds per feature than 15-bit ranks hold: the
+    packer splits the rank trees into consecutive rank spaces (one pre-pass
+    and segment each, the later ones continuing the running sums); scores
+    and ordinals bit-exact."""
+    from paper_1212_2287_b200.synth import complete_flat
+    monkeypatch.setenv("TS_RANK_MIN_DEPTH", "1")
+    rng = np.random.default_rng(123)
+    F, d, T = 4, 10, 200          # ~256 thresholds per feature per tree: ~51k in all
+    n_int = (1 << d) - 1
+    flat = complete_flat(F, d, rng.integers(0, F, (T, n_int)), rng.random((T, n_int)),
+                         rng.standard_normal((T, 1 << d)), weights=rng.uniform(0.5, 1.5, T))
+    ev = _ev(flat)
+    assert ev.model.info["rank_trees"] == T
+    assert ev.model.info["num_segments"] >= 2
+    X = rng.random((3000, F), dtype=np.float32)
+    s, o = oracle.COracle(flat.arrays()).score(X, threads=4, with_ordinals=True)
+    assert np.array_equal(ev.predict_batch(X), s)
+    assert np.array_equal(ev.leaf_indices(X), o.astype(np.int64))
