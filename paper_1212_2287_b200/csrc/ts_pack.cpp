@@ -368,7 +368,7 @@ extern "C" int ts_pack_ex(const ts_model_desc *d, int device, int flags, ts_mode
             if ((layout[t] == kSplit || layout[t] == kComplete) && rank_ok[shapes[t].depth])
                 count[shapes[t].depth]++;
         static const int kRankMinTrees[kRankMaxDepth + 1] = {0, 0, 0, 0, 0, 0, 0, 0,
-                                                             0, 0, 3000, 2500, 500, 150, 300};
+                                                             0, 0, 2000, 1500, 500, 150, 300};
         bool use_d[TS_MAX_DEPTH + 1] = {};
         for (int dd = 1; dd <= kRankMaxDepth; dd++) {
             if (!rank_ok[dd] || !count[dd]) continue;
