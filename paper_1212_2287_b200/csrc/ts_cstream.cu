@@ -40,7 +40,7 @@ bool plan_cstream(int F, int device, CStreamArgs *a) {
     static const Cand cands[] = {{8, 8, 8}, {8, 8, 4}, {4, 8, 8}, {4, 8, 4}, {2, 8, 8},
                                  {2, 8, 4}, {1, 8, 8}, {1, 8, 4}, {4, 16, 8}, {4, 16, 4},
                                  {2, 16, 8}, {2, 16, 4}, {2, 16, 3}, {1, 16, 8}, {1, 16, 4},
-                                 {1, 16, 3}};
+                                 {1, 16, 3}, {1, 16, 2}};
     int fg = 0, fw = 0, fk = 0, ft = 0;
     if (const char *e = getenv("TS_CSTREAM_PLAN")) sscanf(e, "%d,%d,%d,%d", &fg, &fw, &fk, &ft);
     bool found = false;

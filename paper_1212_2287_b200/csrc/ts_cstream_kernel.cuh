@@ -279,15 +279,29 @@ __global__ void __launch_bounds__(threads_c(W), 1) k_cstream(CStreamArgs a) {
                     q[k] = make_uint2(0u, 0u);  // "not on a leaf"
                     v[k] = 0.f;
                 }
+                // Two levels per trip, then leave as soon as every lane of
+                // the warp sits on a leaf in all K chains: the rows' paths
+                // are much shorter than the trees are deep (config 3: 4.8
+                // visits on average in trees 11.6 deep), so the padded
+                // levels of a group are mostly skipped.  le = levels walked.
+                int le = 0;
 #pragma unroll 1
-                for (int l = 0; l < dmax; l++) {
+                while (le < dmax) {
 #pragma unroll
-                    for (int k = 0; k < kK; k++) {
-                        walk_loads(q[k], v[k], p[k], xr, leafmark);
-                        const bool c = v[k] >= __uint_as_float(q[k].y);
-                        p[k] = child_addr(q[k].x, c ? tb8[k] : tb[k]);
-                        if constexpr (ORD) ob[k] = 2u * ob[k] + (c ? 1u : 0u);
+                    for (int h = 0; h < 2; h++) {
+#pragma unroll
+                        for (int k = 0; k < kK; k++) {
+                            walk_loads(q[k], v[k], p[k], xr, leafmark);
+                            const bool c = v[k] >= __uint_as_float(q[k].y);
+                            p[k] = child_addr(q[k].x, c ? tb8[k] : tb[k]);
+                            if constexpr (ORD) ob[k] = 2u * ob[k] + (c ? 1u : 0u);
+                        }
                     }
+                    le += 2;
+                    uint32_t qmin = q[0].x;
+#pragma unroll
+                    for (int k = 1; k < kK; k++) qmin = min(qmin, q[k].x);
+                    if (!__any_sync(0xffffffffu, qmin < leafmark)) break;
                 }
                 if (!waited) {
                     mbar_wait(lbe + b, ((it >> 1) - 1) & 1);
@@ -303,7 +317,7 @@ __global__ void __launch_bounds__(threads_c(W), 1) k_cstream(CStreamArgs a) {
                         if constexpr (ORD) {
                             if (walk_valid)
                                 a.ord[(long long)(tree0 + rel[k]) * a.ld_ord + walk_row] =
-                                    (uint16_t)(ob[k] >> (dmax - dk[k]));
+                                    (uint16_t)(le >= dk[k] ? ob[k] >> (le - dk[k]) : ob[k] << (dk[k] - le));
                         }
                     }
                 }

@@ -13,6 +13,7 @@ cudaError_t launch_w16(const CStreamArgs &a, int device, cudaStream_t stream) {
     if (a.B == 64 && a.k == 3) return launch_kgw<3, 2, 16>(a, device, stream);
     if (a.B == 32 && a.k == 4) return launch_kgw<4, 1, 16>(a, device, stream);
     if (a.B == 32 && a.k == 3) return launch_kgw<3, 1, 16>(a, device, stream);
+    if (a.B == 32 && a.k == 2) return launch_kgw<2, 1, 16>(a, device, stream);
     return cudaErrorInvalidConfiguration;
 }
 

@@ -280,6 +280,14 @@ struct StreamArgs {
     int splits;
     double *leaf_out;
     long long leaf_T;
+    // Tree split, per (32-row block, split CTA): the CTA's own sequential sum
+    // of its terms and the largest / smallest nonzero |leaf| bit pattern it
+    // saw ([row / 32][split][row % 32]; part_key: max then min-1, 2 x 32 per
+    // split).  k_fold uses them to prove that every partial sum of the row is
+    // exactly representable -- then the sum does not depend on the order and
+    // the splits' sums simply add up (ts_stream.cu).
+    double *part_sum;
+    uint32_t *part_key;
     uint32_t lb_bytes;  // warp-split kernel (k_stream_ws): two tpc x 32 fp32 leaf buffers
     int ws_ctas;        // warp-split kernel: CTAs per SM (2 or 3)
     int k;              // k_stream lockstep chains per thread (chains_for_depth / _fallback)

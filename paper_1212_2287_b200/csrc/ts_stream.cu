@@ -169,17 +169,90 @@ __device__ __forceinline__ void fold_load(double *dst, const double *src, int tr
     asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
-// One CTA per 32 rows: all 8 warps pull the rows' f64 terms (w * leaf, already
-// rounded by the walk) into double-buffered shared tiles with cp.async; warp 0
-// adds them, one lane per row, in tree order -- a bare DADD chain.
-__global__ void __launch_bounds__(256) k_fold(const double *terms, long long T,
-                                              int accumulate, double *out, long long n) {
+// Exactness test of a row's tree-split sum.  The terms of a unit-weight
+// ensemble are fp32 leaf values: every term is a multiple of 2^q, q the LSB
+// exponent of the smallest nonzero |leaf|, and any sum of them (and of the
+// running sum acc0 the segment continues from) stays below 2^m, m from the
+// largest |leaf| and the term count.  If m - q <= 53 every partial sum, in
+// ANY order, is exactly representable in f64: no addition rounds, so the
+// reference's tree-order sum (ref evaluators.py:529-535) equals the plain sum
+// of the splits' own sums.  kmax / kmin1: largest |leaf| bit pattern and
+// smallest nonzero one minus 1 (0xffffffff: no nonzero term).  Otherwise
+// (wide dynamic range, non-unit weights) the caller adds the stored terms one
+// by one in tree order.
+__device__ __forceinline__ bool split_sum_exact(uint32_t kmax, uint32_t kmin1, long long T,
+                                                double acc0) {
+    if (kmin1 == 0xffffffffu) return !(acc0 == 0.0 && signbit(acc0));  // all terms are zeros
+    if (kmax >= 0x7f800000u) return false;  // non-unit weights (or a non-finite leaf)
+    const int emax = max((int)(kmax >> 23), 1), emin = max((int)((kmin1 + 1u) >> 23), 1);
+    const int L = 64 - __clzll(T);               // T < 2^L
+    int m = emax - 126 + L;                      // sum of all |terms| < 2^m
+    int q = emin - 150;                          // every term is a multiple of 2^q
+    if (acc0 != 0.0) {
+        const unsigned long long b = (unsigned long long)__double_as_longlong(acc0);
+        const int ea = (int)((b >> 52) & 0x7ff);
+        if (ea == 0 || ea == 0x7ff) return false;  // subnormal, inf, nan: take the slow path
+        const unsigned long long mant = (b & 0xfffffffffffffull) | (1ull << 52);
+        q = min(q, ea - 1075 + (__ffsll((long long)mant) - 1));
+        m = max(m, ea - 1022) + 1;               // |acc0| < 2^(ea - 1022)
+    } else if (signbit(acc0)) {
+        return false;                            // -0.0 + (+0.0 sums): sign depends on the order
+    }
+    return m - q <= 53;
+}
+
+// One CTA per 32 rows.  Fast path (warp 0, one lane per row): add the splits'
+// own sums when split_sum_exact proves the order cannot matter.  Otherwise
+// all 8 warps pull the rows' f64 terms (w * leaf, already rounded by the walk)
+// into double-buffered shared tiles with cp.async and warp 0 adds them, one
+// lane per row, in tree order -- a bare DADD chain.
+__global__ void __launch_bounds__(256) k_fold(const double *terms, long long T, int accumulate,
+                                              double *out, long long n, const double *part_sum,
+                                              const uint32_t *part_key, int splits,
+                                              int no_fast) {
     __shared__ __align__(16) double tile[2][kFoldTrees * 32];
     const long long blk = blockIdx.x;
     const long long row = blk * 32 + (threadIdx.x & 31);
     const double *src = terms + blk * T * 32;
     double acc = 0.0;
-    if (threadIdx.x < 32 && accumulate && row < n) acc = out[row];
+    int done = 0;
+    if (!no_fast) {
+        // all 8 warps fetch the splits' partials (one round trip), warp 0 decides
+        const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        double sum = 0.0;
+        uint32_t kmax = 0u, kmin1 = 0xffffffffu;
+        const double *ps = part_sum + blk * splits * 32 + lane;
+        const uint32_t *pk = part_key + blk * splits * 64 + lane;
+#pragma unroll 8
+        for (int j = w; j < splits; j += 8) {
+            sum = __dadd_rn(sum, ps[j * 32]);
+            kmax = max(kmax, pk[j * 64]);
+            kmin1 = min(kmin1, pk[j * 64 + 32]);
+        }
+        double *rs = tile[0];                                   // [8][32] sums
+        uint32_t *rk = reinterpret_cast<uint32_t *>(tile[0] + 256);  // [8][2][32] keys
+        rs[threadIdx.x] = sum;
+        rk[w * 64 + lane] = kmax;
+        rk[w * 64 + 32 + lane] = kmin1;
+        __syncthreads();
+        if (w == 0) {
+            const bool valid = row < n;
+            if (accumulate && valid) acc = out[row];
+#pragma unroll
+            for (int u = 1; u < 8; u++) {
+                sum = __dadd_rn(sum, rs[u * 32 + lane]);
+                kmax = max(kmax, rk[u * 64 + lane]);
+                kmin1 = min(kmin1, rk[u * 64 + 32 + lane]);
+            }
+            bool ok = !valid || split_sum_exact(kmax, kmin1, T, acc);
+            ok = __all_sync(0xffffffffu, ok);
+            if (ok && valid) out[row] = __dadd_rn(acc, sum);
+            done = ok ? 1 : 0;
+        }
+    } else if (threadIdx.x < 32 && accumulate && row < n) {
+        acc = out[row];
+    }
+    if (__syncthreads_or(done)) return;  // warp 0's verdict; also fences tile[0] before the loads
     const int ntile = (int)((T + kFoldTrees - 1) / kFoldTrees);
     fold_load(tile[0], src, (int)min(T, (long long)kFoldTrees));
     for (int i = 0; i < ntile; i++) {
@@ -250,7 +323,10 @@ cudaError_t launch_stream(int D, const StreamArgs &a0, int device, cudaStream_t 
             return stream_detail::kWsTable[D](w, device, stream);
     }
     const long long blocks = (a.n + 31) / 32;
-    const size_t scratch_bytes = (size_t)blocks * 32 * (size_t)T * sizeof(double);
+    // terms, then each split's own sum and leaf-magnitude keys (StreamArgs::part_sum)
+    const size_t term_bytes = (size_t)blocks * 32 * (size_t)T * sizeof(double);
+    const size_t psum_bytes = (size_t)blocks * std::max(splits, 1) * 32 * sizeof(double);
+    const size_t scratch_bytes = term_bytes + 2 * psum_bytes;
     if (splits < 2 || a.pipe.flags_in || a.pipe.sums_out || scratch_bytes > (256u << 20)) {
         // Wave tail: when the last wave of tiles would leave more than half
         // the CTA slots idle, the full waves run here and the remaining rows
@@ -304,11 +380,18 @@ cudaError_t launch_stream(int D, const StreamArgs &a0, int device, cudaStream_t 
     w.splits = splits;
     w.leaf_out = scratch;
     w.leaf_T = T;
+    w.part_sum = reinterpret_cast<double *>(reinterpret_cast<unsigned char *>(scratch) + term_bytes);
+    w.part_key = reinterpret_cast<uint32_t *>(reinterpret_cast<unsigned char *>(scratch) +
+                                              term_bytes + psum_bytes);
     w.out = nullptr;
     w.accumulate = 0;
     e = stream_detail::kStreamTable[D](w, device, stream);
     if (e == cudaSuccess) {
-        k_fold<<<(unsigned)blocks, 256, 0, stream>>>(scratch, T, a.accumulate, a.out, a.n);
+        // TS_FOLD_FAST=0: always the tree-order chain (A/B experiments, tests)
+        const char *ff = getenv("TS_FOLD_FAST");
+        const int no_fast = ff && atoi(ff) == 0 ? 1 : 0;
+        k_fold<<<(unsigned)blocks, 256, 0, stream>>>(scratch, T, a.accumulate, a.out, a.n,
+                                                     w.part_sum, w.part_key, splits, no_fast);
         count_launch();
         e = cudaGetLastError();
     }

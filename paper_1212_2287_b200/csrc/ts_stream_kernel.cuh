@@ -169,6 +169,31 @@ __device__ __forceinline__ void stage_rows(const StreamArgs &a, float *xs, long 
     if (((F & 3) == 0) && ((a.ld & 3) == 0) && ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0)) {
         const float4 *x4 = reinterpret_cast<const float4 *>(xrow);
         int c = 0;
+        if (a.splits > 1) {
+            // tree-split CTAs walk a few trees each, so the staging round
+            // trips are their critical path: 12 float4 in flight per thread
+            // (a 136-feature row in 3 trips instead of 9)
+            constexpr int U = 12;
+            const int F4 = F >> 2;
+            for (int c0 = 0; c0 < F4; c0 += U) {
+                float4 v[U];
+#pragma unroll
+                for (int u = 0; u < U; u++)
+                    v[u] = (valid && c0 + u < F4) ? __ldg(x4 + c0 + u) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    if (c0 + u >= F4) break;
+                    bad |= !(finite_f(v[u].x) && finite_f(v[u].y) && finite_f(v[u].z) &&
+                             finite_f(v[u].w));
+                    float *dst = xs + 4 * (c0 + u) * kB + r;
+                    dst[0] = v[u].x;
+                    dst[kB] = v[u].y;
+                    dst[2 * kB] = v[u].z;
+                    dst[3 * kB] = v[u].w;
+                }
+            }
+            c = F;
+        }
         for (; c + 16 <= F; c += 16) {
             float4 v[4];
 #pragma unroll
@@ -301,6 +326,9 @@ template <int KP>
 struct LeafPend {
     float lv[KP];
     int t = 0, n = 0;  // first tree, count
+    // tree-split mode: largest |leaf| bit pattern and smallest nonzero one
+    // minus 1 among this thread's trees (see StreamArgs::part_key)
+    uint32_t kmax = 0u, kmin1 = 0xffffffffu;
 };
 template <int D, int FW, bool UNIT_W, int KP>
 __device__ __forceinline__ void flush_leaves(LeafPend<KP> &pend, double &acc, const StreamArgs &a) {
@@ -441,6 +469,14 @@ __device__ __forceinline__ void walk_group(uint32_t tree0, uint32_t xr, double &
             if (!TERMS && a.leaf_out && valid)
                 a.leaf_out[((row >> 5) * a.leaf_T + (t + k - a.t0)) * 32 + (row & 31)] =
                     UNIT_W ? (double)lv : __dmul_rn(__ldg(a.weight + t + k), (double)lv);
+            if constexpr (!TERMS) {
+                if (a.leaf_out) {
+                    // fp32-valued terms only: w * leaf has a full f64 mantissa
+                    const uint32_t key = UNIT_W ? (__float_as_uint(lv) & 0x7fffffffu) : 0x7fffffffu;
+                    pend->kmax = max(pend->kmax, key);
+                    pend->kmin1 = min(pend->kmin1, key - 1u);  // zero wraps to the top: ignored
+                }
+            }
         }
     }
 }
@@ -543,6 +579,14 @@ __global__ void __launch_bounds__(Shape<CW>::kThreads, Shape<CW>::kCtasPerSm)
             }
         }
         if constexpr (SplitRec<D, FW>::kGLeaf) flush_leaves<D, FW, UNIT_W, K>(pend, acc, a);
+        if constexpr (ORD) {
+            if (a.leaf_out && valid) {  // tree-split mode: this CTA's partials (StreamArgs::part_sum)
+                const long long pj = (row >> 5) * a.splits + blockIdx.x / ntiles;
+                a.part_sum[pj * 32 + (row & 31)] = acc;
+                a.part_key[pj * 64 + (row & 31)] = pend.kmax;
+                a.part_key[pj * 64 + 32 + (row & 31)] = pend.kmin1;
+            }
+        }
         if (a.pipe.sums_out) {
             // publish to the next rank (peer memory over NVLink), then flag
             if (valid) a.pipe.sums_out[row] = acc;

@@ -356,6 +356,74 @@ def test_small_batch_tree_split(n, split, monkeypatch):
     assert np.array_equal(ev.leaf_indices(x), o.astype(np.int64))
 
 
+def _leaf_table(kind, rng, T, d):
+    """Leaf values that steer the tree split's fold: 'narrow' lets it prove the
+    sum order-independent (fast path); the others must take the tree-order
+    chain (dynamic range beyond what f64 holds exactly) or sit on its edges."""
+    L = 1 << d
+    if kind == "narrow":
+        return rng.standard_normal((T, L)) * 0.1
+    if kind == "wide":          # 40 decades: partial sums round, order matters
+        return rng.standard_normal((T, L)) * 10.0 ** rng.uniform(-30, 10, (T, L))
+    if kind == "cancel":        # big +/- pairs around tiny odd multiples of 2^-60
+        v = np.where(rng.random((T, L)) < 0.5, 1.0, -1.0) * 2.0 ** rng.integers(20, 30, (T, L))
+        tiny = rng.integers(1, 1 << 20, (T, L)) * 2.0 ** -60
+        return np.where(rng.random((T, L)) < 0.5, v, tiny)
+    if kind == "zeros":         # signed zeros, denormals and a few ordinary values
+        v = rng.choice(np.array([0.0, -0.0, 1e-45, -3e-42, 0.25, -1.5], np.float64), (T, L))
+        return v
+    if kind == "allnegzero":
+        return np.full((T, L), -0.0)
+    raise ValueError(kind)
+
+
+@pytest.mark.parametrize("kind", ["narrow", "wide", "cancel", "zeros", "allnegzero"])
+@pytest.mark.parametrize("n", [1, 77, 1000])
+def test_tree_split_fold_fast_path(kind, n, monkeypatch):
+    """Unit-weight ensembles: the fold adds the splits' own sums when the
+    leaves' dynamic range proves every partial sum exact (ts_stream.cu
+    split_sum_exact), else the tree-order chain; both must give the
+    reference's sequential f64 sum bit for bit (ref evaluators.py:529-535)."""
+    from paper_1212_2287_b200.synth import complete_flat
+    rng = np.random.default_rng(len(kind) * 1000 + n)
+    T, d, F = 400, 7, 40
+    n_int = (1 << d) - 1
+    flat = complete_flat(F, d, rng.integers(0, F, (T, n_int)), rng.random((T, n_int)),
+                         _leaf_table(kind, rng, T, d))
+    x = rng.random((n, F), dtype=np.float32)
+    ref = oracle.COracle(flat.arrays()).score(x, threads=4)
+    got = {}
+    for fast in ("1", "0"):
+        monkeypatch.setenv("TS_FOLD_FAST", fast)
+        for split in ("3", "11"):
+            monkeypatch.setenv("TS_SPLIT", split)
+            ev = _ev(flat)
+            got[fast, split] = ev.predict_batch(x)
+            ev.close()
+    for k, v in got.items():
+        assert np.array_equal(v.view(np.uint64), ref.view(np.uint64)), k
+
+
+def test_tree_split_fold_continues_running_sum(monkeypatch):
+    """Unit-weight segments of different depths: the second segment's fold
+    starts from the first one's sums (acc0 != 0 in the exactness test), also
+    when those are too fine-grained for the fast path."""
+    from paper_1212_2287_b200 import Ensemble
+    monkeypatch.setenv("TS_SPLIT", "5")
+    for scale in (1.0, 2.0 ** -45):
+        rng = np.random.default_rng(91)
+        f = 40
+        trees = [(_rand_complete(rng, 6, f, leaf_scale=scale), 1.0) for _ in range(150)]
+        trees += [(_rand_complete(rng, 8, f), 1.0) for _ in range(150)]
+        ens = Ensemble(f, trees)
+        X = rng.random((300, f), dtype=np.float32)
+        s = oracle.COracle(ens.flat().arrays()).score(X, threads=4)
+        ev = _ev(ens)
+        assert ev.model.info["num_segments"] == 2
+        assert np.array_equal(ev.predict_batch(X).view(np.uint64), s.view(np.uint64))
+        ev.close()
+
+
 @pytest.mark.parametrize("name", ["complete_d6", "ties_counts", "trivia"])
 def test_complete_trees_on_irregular_kernel(name, monkeypatch):
     """TS_FORCE_CSTREAM packs complete trees as child-index records for the
@@ -439,12 +507,12 @@ def _rand_unbalanced(rng, max_depth, f, prune=0.35):
     return Tree(build_node(0))
 
 
-def _rand_complete(rng, depth, f):
+def _rand_complete(rng, depth, f, leaf_scale=1.0):
     from paper_1212_2287_b200 import Node, Tree
 
     def build_node(level):
         if level == depth:
-            return Node.leaf(rng.standard_normal())
+            return Node.leaf(rng.standard_normal() * leaf_scale)
         return Node.internal(int(rng.integers(f)), rng.random(), build_node(level + 1),
                              build_node(level + 1))
     return Tree(build_node(0))
