@@ -170,34 +170,38 @@ __device__ __forceinline__ void fold_load(double *dst, const double *src, int tr
 }
 
 // Exactness test of a row's tree-split sum.  The terms of a unit-weight
-// ensemble are fp32 leaf values: every term is a multiple of 2^q, q the LSB
-// exponent of the smallest nonzero |leaf|, and any sum of them (and of the
-// running sum acc0 the segment continues from) stays below 2^m, m from the
-// largest |leaf| and the term count.  If m - q <= 53 every partial sum, in
-// ANY order, is exactly representable in f64: no addition rounds, so the
-// reference's tree-order sum (ref evaluators.py:529-535) equals the plain sum
-// of the splits' own sums.  kmax / kmin1: largest |leaf| bit pattern and
-// smallest nonzero one minus 1 (0xffffffff: no nonzero term).  Otherwise
-// (wide dynamic range, non-unit weights) the caller adds the stored terms one
-// by one in tree order.
-__device__ __forceinline__ bool split_sum_exact(uint32_t kmax, uint32_t kmin1, long long T,
-                                                double acc0) {
-    if (kmin1 == 0xffffffffu) return !(acc0 == 0.0 && signbit(acc0));  // all terms are zeros
-    if (kmax >= 0x7f800000u) return false;  // non-unit weights (or a non-finite leaf)
-    const int emax = max((int)(kmax >> 23), 1), emin = max((int)((kmin1 + 1u) >> 23), 1);
-    const int L = 64 - __clzll(T);               // T < 2^L
-    int m = emax - 126 + L;                      // sum of all |terms| < 2^m
-    int q = emin - 150;                          // every term is a multiple of 2^q
+// ensemble are fp32 leaf values: every term, and so every partial sum, is a
+// multiple of 2^q, q the LSB exponent of the smallest nonzero |leaf| (and of
+// the running sum acc0 the segment continues from).  M bounds every partial
+// sum the tree-order chain or the splits can form: |acc0| plus the largest
+// |running sum| each split reached (amax, rounded up).  If M < 2^m with
+// m - q <= 53, every one of those sums is exactly representable in f64: no
+// addition rounds, so the reference's tree-order sum (ref
+// evaluators.py:529-535) equals the plain sum of the splits' own sums.
+// kmin1: smallest nonzero |leaf| bit pattern minus 1 (0xffffffff: no nonzero
+// term).  Otherwise (wide dynamic range; non-unit weights send amax = all
+// ones, i.e. M = NaN) the caller adds the terms one by one in tree order.
+__device__ __forceinline__ double amax_bound(uint32_t amax) {
+    // >= the |sum| whose high word is amax; all ones (non-unit weights) and
+    // anything at the top of the range: infinity, which fails the test
+    return amax >= 0x7fe00000u ? INFINITY : __hiloint2double((int)(amax + 1u), 0);
+}
+__device__ __forceinline__ bool split_sum_exact(double M, uint32_t kmin1, double acc0) {
+    if (kmin1 == 0xffffffffu) return !(acc0 == 0.0 && signbit(acc0)) && M < INFINITY;  // all terms zero
+    int q = max((int)((kmin1 + 1u) >> 23), 1) - 150;  // every term is a multiple of 2^q
     if (acc0 != 0.0) {
         const unsigned long long b = (unsigned long long)__double_as_longlong(acc0);
         const int ea = (int)((b >> 52) & 0x7ff);
         if (ea == 0 || ea == 0x7ff) return false;  // subnormal, inf, nan: take the slow path
         const unsigned long long mant = (b & 0xfffffffffffffull) | (1ull << 52);
         q = min(q, ea - 1075 + (__ffsll((long long)mant) - 1));
-        m = max(m, ea - 1022) + 1;               // |acc0| < 2^(ea - 1022)
     } else if (signbit(acc0)) {
-        return false;                            // -0.0 + (+0.0 sums): sign depends on the order
+        return false;                              // -0.0 + (+0.0 sums): sign depends on the order
     }
+    const double Mt = M + fabs(acc0);
+    if (!(Mt < INFINITY)) return false;
+    const int em = (int)(((unsigned long long)__double_as_longlong(Mt) >> 52) & 0x7ff);
+    const int m = em - 1022 + 1;                   // Mt < 2^(em - 1022); one more for M's own rounding
     return m - q <= 53;
 }
 
@@ -219,21 +223,22 @@ __global__ void __launch_bounds__(256) k_fold(const double *terms, long long T, 
     if (!no_fast) {
         // all 8 warps fetch the splits' partials (one round trip), warp 0 decides
         const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-        double sum = 0.0;
-        uint32_t kmax = 0u, kmin1 = 0xffffffffu;
+        double sum = 0.0, M = 0.0;
+        uint32_t kmin1 = 0xffffffffu;
         const double *ps = part_sum + blk * splits * 32 + lane;
         const uint32_t *pk = part_key + blk * splits * 64 + lane;
 #pragma unroll 8
         for (int j = w; j < splits; j += 8) {
             sum = __dadd_rn(sum, ps[j * 32]);
-            kmax = max(kmax, pk[j * 64]);
+            M += amax_bound(pk[j * 64]);
             kmin1 = min(kmin1, pk[j * 64 + 32]);
         }
-        double *rs = tile[0];                                   // [8][32] sums
-        uint32_t *rk = reinterpret_cast<uint32_t *>(tile[0] + 256);  // [8][2][32] keys
+        double *rs = tile[0];                                        // [8][32] sums
+        double *rm = tile[0] + 256;                                  // [8][32] magnitude bounds
+        uint32_t *rk = reinterpret_cast<uint32_t *>(tile[0] + 512);  // [8][32] keys
         rs[threadIdx.x] = sum;
-        rk[w * 64 + lane] = kmax;
-        rk[w * 64 + 32 + lane] = kmin1;
+        rm[threadIdx.x] = M;
+        rk[threadIdx.x] = kmin1;
         __syncthreads();
         if (w == 0) {
             const bool valid = row < n;
@@ -241,10 +246,10 @@ __global__ void __launch_bounds__(256) k_fold(const double *terms, long long T, 
 #pragma unroll
             for (int u = 1; u < 8; u++) {
                 sum = __dadd_rn(sum, rs[u * 32 + lane]);
-                kmax = max(kmax, rk[u * 64 + lane]);
-                kmin1 = min(kmin1, rk[u * 64 + 32 + lane]);
+                M += rm[u * 32 + lane];
+                kmin1 = min(kmin1, rk[u * 32 + lane]);
             }
-            bool ok = !valid || split_sum_exact(kmax, kmin1, T, acc);
+            bool ok = !valid || split_sum_exact(M, kmin1, acc);
             ok = __all_sync(0xffffffffu, ok);
             if (ok && valid) out[row] = __dadd_rn(acc, sum);
             done = ok ? 1 : 0;
@@ -275,7 +280,167 @@ __global__ void __launch_bounds__(256) k_fold(const double *terms, long long T, 
     }
     if (threadIdx.x < 32 && row < n) out[row] = acc;
 }
+// Balanced tree split, second kernel: one CTA per tile.  A tile shared by
+// several walking CTAs (StreamArgs::sk_ctas) has one partial per CTA; a row
+// whose partial sums provably cannot round (split_sum_exact) gets their sum,
+// which then IS the tree-order sum.  Any other row (non-unit weights, a wide
+// leaf range) is added up here in tree order from the per-tree leaf ordinals
+// the walk stored (2 bytes per tree and row instead of an 8-byte term): the
+// leaf values come from the model blob (kSplit record: leaves at leaf0 of each
+// tree_bytes record), term = w * leaf rounded to f64, then the add -- the
+// walk's own arithmetic (ref evaluators.py:529-535).
+// kCombineThreads / B threads fetch each row's partials.
+constexpr int kCombineThreads = 512;
+constexpr int kCombineWarps = kCombineThreads / 32;
+constexpr int kCombineStep = 128;  // terms a warp fetches per step of a row's tree-order chain
+__global__ void __launch_bounds__(kCombineThreads)
+    k_combine(const double *part_sum, const uint32_t *part_key, int slices, int B,
+              long long ntiles, int nchunks, int ctas, long long T, int accumulate, double *out,
+              long long n, const uint16_t *ord, long long ld_ord, const unsigned char *seg,
+              uint32_t tree_bytes, uint32_t leaf0, const double *weight, int no_fast) {
+    __shared__ double rs[kCombineThreads];
+    __shared__ double rm[kCombineThreads];
+    __shared__ uint32_t rk[kCombineThreads];
+    __shared__ double terms[kCombineWarps][kCombineStep];
+    __shared__ int slow_rows[256];
+    __shared__ int n_slow;
+    const long long tile = blockIdx.x;
+    const long long W = ntiles * nchunks;
+    const long long b0 = ((tile * nchunks + 1) * ctas - 1) / W;
+    const long long b1 = ((tile + 1) * nchunks * ctas - 1) / W;
+    const int cnt = (int)(b1 - b0 + 1);
+    if (cnt == 1) return;  // walked whole by one CTA, which wrote the scores
+    const int r = threadIdx.x % B, p = threadIdx.x / B, P = kCombineThreads / B;
+    const long long row = tile * B + r;
+    const bool valid = row < n;
+    if (threadIdx.x == 0) n_slow = 0;
+    double sum = 0.0, M = 0.0;
+    uint32_t kmin1 = 0xffffffffu;
+    if (valid) {
+#pragma unroll 4
+        for (int j = p; j < cnt; j += P) {
+            const long long pj = (tile * slices + j) * B + r;
+            sum = __dadd_rn(sum, part_sum[pj]);
+            const uint2 k = *reinterpret_cast<const uint2 *>(part_key + 2 * pj);
+            M += amax_bound(k.x);
+            kmin1 = min(kmin1, k.y);
+        }
+    }
+    rs[threadIdx.x] = sum;
+    rm[threadIdx.x] = M;
+    rk[threadIdx.x] = kmin1;
+    __syncthreads();
+    if (p == 0 && valid) {
+        for (int u = 1; u < P; u++) {
+            sum = __dadd_rn(sum, rs[u * B + r]);
+            M += rm[u * B + r];
+            kmin1 = min(kmin1, rk[u * B + r]);
+        }
+        const double acc = accumulate ? out[row] : 0.0;
+        if (!no_fast && split_sum_exact(M, kmin1, acc)) out[row] = __dadd_rn(acc, sum);
+        else slow_rows[atomicAdd(&n_slow, 1)] = r;
+    }
+    __syncthreads();
+    // Rows whose sums could round: one warp per row.  The lanes fetch the
+    // row's leaf values kCombineStep trees at a time (ordinal, then leaf: two
+    // dependent loads, all in flight together) while lane 0 adds the previous
+    // step's terms in tree order.
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int U = kCombineStep / 32;
+    for (int i = warp; i < n_slow; i += kCombineWarps) {
+        const long long srow = tile * B + slow_rows[i];
+        const uint16_t *o = ord + srow;
+        double acc = accumulate ? out[srow] : 0.0;
+        double nx[U];
+        auto fetch = [&](long long t0) {
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const long long t = t0 + u * 32 + lane;
+                nx[u] = 0.0;
+                if (t < T) {
+                    const float lv = __ldg(reinterpret_cast<const float *>(seg + t * tree_bytes + leaf0) +
+                                           __ldg(o + t * ld_ord));
+                    nx[u] = weight ? __dmul_rn(__ldg(weight + t), (double)lv) : (double)lv;
+                }
+            }
+        };
+        fetch(0);
+        for (long long t0 = 0; t0 < T; t0 += kCombineStep) {
+#pragma unroll
+            for (int u = 0; u < U; u++) terms[warp][u * 32 + lane] = nx[u];
+            __syncwarp();
+            if (t0 + kCombineStep < T) fetch(t0 + kCombineStep);
+            if (lane == 0) {
+                const int nt = (int)min((long long)kCombineStep, T - t0);
+#pragma unroll 8
+                for (int k = 0; k < nt; k++) acc = __dadd_rn(acc, terms[warp][k]);
+            }
+            __syncwarp();
+        }
+        if (lane == 0) out[srow] = acc;
+    }
+}
 }  // namespace
+
+// Balanced tree split ("stream-K"): batches of less than a few waves of tiles
+// -- where whole-tile CTAs leave SMs idle or a last partial wave costs a whole
+// one -- are cut into `ctas` equal runs of (tile, chunk) items
+// (StreamArgs::sk_ctas).  Two launches: the walk (which also stores each
+// tree's leaf ordinal, into the caller's buffer or scratch) and k_combine.
+static cudaError_t launch_balanced(int D, const StreamArgs &a, int ctas, long long tiles,
+                                   int nchunks, int device, cudaStream_t stream) {
+    const int B = 32 * a.cw;
+    const int T = a.t1 - a.t0;
+    const int slices = (int)((ctas + tiles - 1) / tiles) + 1;
+    const size_t psum_bytes = (size_t)tiles * slices * B * sizeof(double);
+    const long long ld_ord = a.ord ? a.ld_ord : ((a.n + 63) & ~63ll);
+    const size_t ord_bytes = a.ord ? 0 : (size_t)T * ld_ord * sizeof(uint16_t);
+    cudaMemPool_t pool = scratch_pool(device);
+    if (!pool || ord_bytes > (128u << 20)) return cudaErrorNotSupported;
+    unsigned char *scratch = nullptr;
+    cudaError_t e = cudaMallocFromPoolAsync((void **)&scratch, 2 * psum_bytes + ord_bytes, pool, stream);
+    if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        return cudaErrorNotSupported;  // the caller goes on to the other kernels
+    }
+    StreamArgs w = a;
+    float *xcopy = nullptr;
+    if (a.x_mapped) {
+        // CTAs sharing a tile each read its rows: not over PCIe
+        e = x_device_copy(a.x, a.n, a.ld, device, stream, &xcopy);
+        if (e != cudaSuccess) {
+            cudaFreeAsync(scratch, stream);
+            return e;
+        }
+        if (xcopy) w.x = xcopy;
+    }
+    w.sk_ctas = ctas;
+    w.sk_slices = slices;
+    w.part_sum = reinterpret_cast<double *>(scratch);
+    w.part_key = reinterpret_cast<uint32_t *>(scratch + psum_bytes);
+    if (!a.ord) {
+        // the walk indexes ordinals by absolute tree number
+        w.ord = reinterpret_cast<uint16_t *>(scratch + 2 * psum_bytes) - (ptrdiff_t)a.t0 * ld_ord;
+        w.ld_ord = ld_ord;
+    }
+    e = stream_detail::kStreamTable[D](w, device, stream);
+    if (e == cudaSuccess) {
+        const char *ff = getenv("TS_FOLD_FAST");
+        const SplitGeom g = split_geom(D, a.fw);
+        k_combine<<<(unsigned)tiles, kCombineThreads, 0, stream>>>(
+            w.part_sum, w.part_key, slices, B, tiles, nchunks, ctas, T, a.accumulate, a.out, a.n,
+            w.ord + (ptrdiff_t)a.t0 * w.ld_ord, w.ld_ord, a.blob + a.seg_byte0, g.bytes, g.leaf0,
+            a.unit_w ? nullptr : a.weight + a.t0, ff && atoi(ff) == 0 ? 1 : 0);
+        count_launch();
+        e = cudaGetLastError();
+    }
+    cudaError_t f = cudaFreeAsync(scratch, stream);
+    if (xcopy) {
+        const cudaError_t g2 = cudaFreeAsync(xcopy, stream);
+        if (f == cudaSuccess) f = g2;
+    }
+    return e != cudaSuccess ? e : f;
+}
 
 // Small batches leave most SMs idle (one CTA walks ALL trees of its tile), so
 // when the tiles fill less than half of the resident CTA slots the segment's
@@ -301,6 +466,33 @@ cudaError_t launch_stream(int D, const StreamArgs &a0, int device, cudaStream_t 
     if (const char *e = getenv("TS_SPLIT")) {
         const int f = atoi(e);
         splits = f <= 0 ? 1 : std::min(f, nchunks);
+    }
+    // Balanced tree split (launch_balanced) where it measured faster
+    // (profiles/r2_balanced_split.txt, 1000 trees): unit weights, depth 7-9,
+    // a walk long enough to carry the second launch, and tiles filling
+    // between ~0.3 and ~0.7 of the resident CTA slots -- below that the
+    // uniform split / warp-split kernels win, above it one wave of whole
+    // tiles does (d = 8, T = 1000: n = 12k 87 -> 66 us, 16k 105 -> 82, 20k
+    // 124 -> 99; d = 9: 14k 122 -> 88, 22k 152 -> 126; T = 4000: 10k 336 ->
+    // 184).  Depths <= 6 and >= 10 pay more for the per-tree ordinal store
+    // than the balance returns.  TS_SK=1 forces it (any weights, any shape),
+    // TS_SK=0 disables it; TS_SK_CTAS overrides the CTA count (tests, A/B).
+    {
+        const char *ske = getenv("TS_SK");
+        const double fill = (double)tiles / resident;
+        bool sk = a.unit_w && long_walk && D >= 7 && D <= 9 && T <= 4096 &&
+                  (long long)T * D >= 6000 && fill >= (D == 7 ? 0.45 : 0.27) && fill <= 0.72 &&
+                  !getenv("TS_SPLIT") && !getenv("TS_WS");
+        if (ske) sk = atoi(ske) != 0;
+        if (sk && !a.pipe.flags_in && !a.pipe.sums_out) {
+            const long long W = tiles * nchunks;
+            long long ctas = std::min<long long>(resident, W);
+            if (const char *ce = getenv("TS_SK_CTAS")) ctas = std::min<long long>(std::max(1, atoi(ce)), W);
+            if (ctas > tiles || tiles % ctas != 0) {
+                const cudaError_t e = launch_balanced(D, a, (int)ctas, tiles, nchunks, device, stream);
+                if (e != cudaErrorNotSupported) return e;
+            }
+        }
     }
     // Warp-split kernel (k_stream_ws) for batches whose 32-row tiles fill at
     // most 1.5 waves of its CTAs and give every SM one (or whose walk is too

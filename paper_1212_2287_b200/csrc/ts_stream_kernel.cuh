@@ -169,7 +169,7 @@ __device__ __forceinline__ void stage_rows(const StreamArgs &a, float *xs, long 
     if (((F & 3) == 0) && ((a.ld & 3) == 0) && ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0)) {
         const float4 *x4 = reinterpret_cast<const float4 *>(xrow);
         int c = 0;
-        if (a.splits > 1) {
+        if (a.splits > 1 || a.sk_ctas > 0) {
             // tree-split CTAs walk a few trees each, so the staging round
             // trips are their critical path: 12 float4 in flight per thread
             // (a 136-feature row in 3 trips instead of 9)
@@ -326,9 +326,10 @@ template <int KP>
 struct LeafPend {
     float lv[KP];
     int t = 0, n = 0;  // first tree, count
-    // tree-split mode: largest |leaf| bit pattern and smallest nonzero one
-    // minus 1 among this thread's trees (see StreamArgs::part_key)
-    uint32_t kmax = 0u, kmin1 = 0xffffffffu;
+    // tree-split modes (StreamArgs::part_key): high word of the largest
+    // |running sum| this thread reached, and the smallest nonzero |leaf| bit
+    // pattern minus 1 among its trees
+    uint32_t amax = 0u, kmin1 = 0xffffffffu;
 };
 template <int D, int FW, bool UNIT_W, int KP>
 __device__ __forceinline__ void flush_leaves(LeafPend<KP> &pend, double &acc, const StreamArgs &a) {
@@ -338,6 +339,8 @@ __device__ __forceinline__ void flush_leaves(LeafPend<KP> &pend, double &acc, co
             const double term = UNIT_W ? (double)pend.lv[j]
                                        : __dmul_rn(__ldg(a.weight + pend.t + j), (double)pend.lv[j]);
             acc = __dadd_rn(acc, term);
+            if (a.leaf_out || a.sk_ctas > 0)
+                pend.amax = max(pend.amax, (uint32_t)__double2hiint(acc) & 0x7fffffffu);
         }
     }
     pend.n = 0;
@@ -359,7 +362,10 @@ __device__ __forceinline__ void flush_leaves(LeafPend<KP> &pend, double &acc, co
 //    goes to the shared leaf buffer at lbt + k * 128 (one 32-row slab per
 //    tree) instead of into acc; the accumulator warp adds w * leaf in tree
 //    order.
-template <int D, int NK, int FW, bool UNIT_W, bool ORD, int CW, bool TERMS = false, int KP = 1>
+// ORD: 0 scores only; 1 also ordinals (a.ord) and / or the tree split's terms
+// (a.leaf_out), checked at run time; 2 balanced tree split of a unit-weight
+// ensemble (a.ord set, partial-sum bookkeeping, no terms).
+template <int D, int NK, int FW, bool UNIT_W, int ORD, int CW, bool TERMS = false, int KP = 1>
 __device__ __forceinline__ void walk_group(uint32_t tree0, uint32_t xr, double &acc,
                                            const StreamArgs &a, int t, long long row,
                                            bool valid, uint32_t lbt = 0,
@@ -460,7 +466,12 @@ __device__ __forceinline__ void walk_group(uint32_t tree0, uint32_t xr, double &
                 UNIT_W ? (double)lv : __dmul_rn(__ldg(a.weight + t + k), (double)lv);
             acc = __dadd_rn(acc, term);
         }
-        if constexpr (ORD) {
+        if constexpr (ORD == 2) {
+            if (valid) a.ord[(long long)(t + k) * a.ld_ord + row] = (uint16_t)(h - (1u << D));
+            pend->kmin1 = min(pend->kmin1, (__float_as_uint(lv) & 0x7fffffffu) - 1u);  // zero wraps: ignored
+            if constexpr (!kDefer)
+                pend->amax = max(pend->amax, (uint32_t)__double2hiint(acc) & 0x7fffffffu);
+        } else if constexpr (ORD == 1) {
             if (a.ord && valid) a.ord[(long long)(t + k) * a.ld_ord + row] = (uint16_t)(h - (1u << D));
             // tree-split mode: [row / 32][tree][row % 32] for k_fold.  Only rows
             // < n: the scratch holds ceil(n / 32) blocks, and a 128-row tile's
@@ -470,18 +481,23 @@ __device__ __forceinline__ void walk_group(uint32_t tree0, uint32_t xr, double &
                 a.leaf_out[((row >> 5) * a.leaf_T + (t + k - a.t0)) * 32 + (row & 31)] =
                     UNIT_W ? (double)lv : __dmul_rn(__ldg(a.weight + t + k), (double)lv);
             if constexpr (!TERMS) {
-                if (a.leaf_out) {
-                    // fp32-valued terms only: w * leaf has a full f64 mantissa
-                    const uint32_t key = UNIT_W ? (__float_as_uint(lv) & 0x7fffffffu) : 0x7fffffffu;
-                    pend->kmax = max(pend->kmax, key);
-                    pend->kmin1 = min(pend->kmin1, key - 1u);  // zero wraps to the top: ignored
+                if (a.leaf_out || a.sk_ctas > 0) {
+                    // fp32-valued terms only (w * leaf has a full f64
+                    // mantissa: amax = all ones makes the exactness test fail)
+                    if constexpr (UNIT_W) {
+                        pend->kmin1 = min(pend->kmin1, (__float_as_uint(lv) & 0x7fffffffu) - 1u);  // zero wraps: ignored
+                        if constexpr (!kDefer)
+                            pend->amax = max(pend->amax, (uint32_t)__double2hiint(acc) & 0x7fffffffu);
+                    } else {
+                        pend->amax = 0xffffffffu;
+                    }
                 }
             }
         }
     }
 }
 
-template <int D, int K, int FW, bool UNIT_W, bool ORD, int CW>
+template <int D, int K, int FW, bool UNIT_W, int ORD, int CW>
 __global__ void __launch_bounds__(Shape<CW>::kThreads, Shape<CW>::kCtasPerSm)
     k_stream(StreamArgs a) {
     constexpr int kB = Shape<CW>::kB;
@@ -504,26 +520,60 @@ __global__ void __launch_bounds__(Shape<CW>::kThreads, Shape<CW>::kCtasPerSm)
     __syncthreads();
     const long long ntiles = (a.n + kB - 1) / kB;
     const int nchunks = (a.t1 - a.t0 + a.tpc - 1) / a.tpc;
-    // Tiles this CTA owns and the chunk range it walks: all chunks of tiles
-    // blockIdx.x, +gridDim.x, ... normally; one tile and 1/splits of the
-    // chunks in small-batch tree-split mode.
-    long long tile0 = blockIdx.x, tstep = gridDim.x;
-    int cb = 0, ce = nchunks;
-    if (a.splits > 1) {
-        tile0 = blockIdx.x % ntiles;
-        tstep = ntiles;
-        const long long j = blockIdx.x / ntiles;
-        cb = (int)(j * nchunks / a.splits);
-        ce = (int)((j + 1) * nchunks / a.splits);
-    }
+    // Spans (a tile and the chunk range [cb, ce) walked of it) this CTA owns:
+    // all chunks of tiles blockIdx.x, +gridDim.x, ... normally; one tile and 1/splits of its chunks in
+    // small-batch tree-split mode; an equal run of the tile-major (tile,
+    // chunk) items in balanced mode (a.sk_ctas), which may end one tile and
+    // start the next.
+    struct Span {
+        long long tile, pos, end;
+        int cb, ce;
+    };
+    auto span_load = [&](Span &sp) -> bool {
+        if (sp.pos >= sp.end) return false;
+        if (a.sk_ctas > 0) {
+            sp.tile = sp.pos / nchunks;
+            sp.cb = (int)(sp.pos - sp.tile * nchunks);
+            sp.ce = (int)min((long long)nchunks, sp.cb + (sp.end - sp.pos));
+        } else if (a.splits > 1) {
+            sp.tile = blockIdx.x % ntiles;
+            const long long j = blockIdx.x / ntiles;
+            sp.cb = (int)(j * nchunks / a.splits);
+            sp.ce = (int)((j + 1) * nchunks / a.splits);
+        } else {
+            sp.tile = sp.pos;
+            sp.cb = 0;
+            sp.ce = nchunks;
+        }
+        return true;
+    };
+    auto span_first = [&](Span &sp) -> bool {
+        if (a.sk_ctas > 0) {
+            const long long W = ntiles * nchunks;
+            sp.pos = (long long)blockIdx.x * W / a.sk_ctas;
+            sp.end = (long long)(blockIdx.x + 1) * W / a.sk_ctas;
+        } else if (a.splits > 1) {
+            sp.pos = 0;
+            sp.end = 1;
+        } else {
+            sp.pos = blockIdx.x;
+            sp.end = ntiles;
+        }
+        return span_load(sp);
+    };
+    auto span_next = [&](Span &sp) -> bool {
+        sp.pos += a.sk_ctas > 0 ? (long long)(sp.ce - sp.cb) : a.splits > 1 ? 1 : (long long)gridDim.x;
+        return span_load(sp);
+    };
 
     if (warp == kConsumerWarps) {  // ---- producer warp: TMA bulk copies
         if (lane == 0) {
             // ring position tracked incrementally (no runtime division)
             int s = 0;
             uint32_t ph = 0, used = 0;  // phase of stage s's next reuse; first lap done?
-            for (long long tile = tile0; tile < ntiles; tile += tstep) {
-                for (int c = cb; c < ce; c++) {
+            Span sp;
+            for (bool more = span_first(sp); more; more = span_next(sp)) {
+                for (int c = sp.cb; c < sp.ce; c++) {
                     if (used) mbar_wait(empty + s, ph);
                     const int trees = min(a.tpc, a.t1 - a.t0 - c * a.tpc);
                     produce_chunk<D, FW>(a, ring + s * a.chunk_cap, full + s, c, trees);
@@ -543,13 +593,18 @@ __global__ void __launch_bounds__(Shape<CW>::kThreads, Shape<CW>::kCtasPerSm)
     const uint32_t xr = su32(xs) + 4u * r;
     int s = 0;
     uint32_t ph = 0;  // parity of stage s's current fill
-    for (long long tile = tile0; tile < ntiles; tile += tstep) {
+    Span sp;
+    for (bool more = span_first(sp); more; more = span_next(sp)) {
+        const long long tile = sp.tile;
+        const int cb = sp.cb, ce = sp.ce;
         const long long row = tile * kB + r;
         const bool valid = row < a.n;
         consumer_sync<kB>();  // previous tile's walks are done with xs
         stage_rows<kB>(a, xs, tile * kB);
         consumer_sync<kB>();
-        double acc = (a.accumulate && valid) ? a.out[row] : 0.0;
+        // balanced mode: a tile walked only in part contributes a partial sum from 0
+        const bool part = a.sk_ctas > 0 && (cb != 0 || ce != nchunks);
+        double acc = (a.accumulate && valid && !part) ? a.out[row] : 0.0;
         LeafPend<K> pend;  // global-leaf depths: the last group's leaves, added late
         // Cross-GPU running-sum pipeline (ts_score_pipe): this warp's 32-row
         // block continues the sums the previous rank published for it.
@@ -583,11 +638,22 @@ __global__ void __launch_bounds__(Shape<CW>::kThreads, Shape<CW>::kCtasPerSm)
             if (a.leaf_out && valid) {  // tree-split mode: this CTA's partials (StreamArgs::part_sum)
                 const long long pj = (row >> 5) * a.splits + blockIdx.x / ntiles;
                 a.part_sum[pj * 32 + (row & 31)] = acc;
-                a.part_key[pj * 64 + (row & 31)] = pend.kmax;
+                a.part_key[pj * 64 + (row & 31)] = pend.amax;
                 a.part_key[pj * 64 + 32 + (row & 31)] = pend.kmin1;
             }
         }
-        if (a.pipe.sums_out) {
+        if (part) {
+            // slice = this CTA's rank among the CTAs sharing the tile (the
+            // first of them holds item tile * nchunks)
+            if (valid) {
+                const long long W = ntiles * nchunks;
+                const long long b0 = ((tile * nchunks + 1) * a.sk_ctas - 1) / W;
+                const long long pj = (tile * a.sk_slices + (blockIdx.x - b0)) * kB + r;
+                a.part_sum[pj] = acc;
+                a.part_key[2 * pj] = pend.amax;
+                a.part_key[2 * pj + 1] = pend.kmin1;
+            }
+        } else if (a.pipe.sums_out) {
             // publish to the next rank (peer memory over NVLink), then flag
             if (valid) a.pipe.sums_out[row] = acc;
             __threadfence_system();
@@ -802,9 +868,10 @@ cudaError_t launch_ws_d(const StreamArgs &a, int device, cudaStream_t stream) {
 
 template <int D, int K, int FW, int CW>
 auto pick_kernel_k(const StreamArgs &a) {
-    if (a.ord || a.leaf_out)
-        return a.unit_w ? k_stream<D, K, FW, true, true, CW> : k_stream<D, K, FW, false, true, CW>;
-    return a.unit_w ? k_stream<D, K, FW, true, false, CW> : k_stream<D, K, FW, false, false, CW>;
+    if (a.sk_ctas > 0 && a.unit_w) return k_stream<D, K, FW, true, 2, CW>;
+    if (a.ord || a.leaf_out || a.sk_ctas > 0)
+        return a.unit_w ? k_stream<D, K, FW, true, 1, CW> : k_stream<D, K, FW, false, 1, CW>;
+    return a.unit_w ? k_stream<D, K, FW, true, 0, CW> : k_stream<D, K, FW, false, 0, CW>;
 }
 template <int D, int FW, int CW>
 auto pick_kernel(const StreamArgs &a) {
@@ -827,9 +894,10 @@ cudaError_t launch_dc(const StreamArgs &a, int device, cudaStream_t stream) {
     e = ensure_smem((const void *)kern, smem);
     if (e != cudaSuccess) return e;
     const long long tiles = (a.n + kB - 1) / kB;
-    const int grid = a.splits > 1 ? (int)(tiles * a.splits)
-                                  : (int)(tiles < (long long)sms * kCtasPerSm
-                                              ? tiles : (long long)sms * kCtasPerSm);
+    const int grid = a.sk_ctas > 0 ? a.sk_ctas
+                     : a.splits > 1 ? (int)(tiles * a.splits)
+                                    : (int)(tiles < (long long)sms * kCtasPerSm
+                                                ? tiles : (long long)sms * kCtasPerSm);
     kern<<<grid, kThreads, smem, stream>>>(a);
     count_launch();
     return cudaGetLastError();

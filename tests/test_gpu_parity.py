@@ -404,6 +404,96 @@ def test_tree_split_fold_fast_path(kind, n, monkeypatch):
         assert np.array_equal(v.view(np.uint64), ref.view(np.uint64)), k
 
 
+@pytest.mark.parametrize("kind", ["narrow", "wide", "cancel", "zeros", "allnegzero"])
+@pytest.mark.parametrize("n,ctas", [(1, None), (300, "7"), (300, None), (5000, None), (5000, "50"),
+                                    (5000, "333")])
+def test_balanced_tree_split(kind, n, ctas, monkeypatch):
+    """Balanced tree split (TS_SK=1; ts_stream.cu launch_balanced): equal runs
+    of (tile, chunk) items per CTA, tiles shared by several CTAs combined from
+    their partial sums when provably exact, re-walked in tree order otherwise
+    -- scores and ordinals identical to the oracle's either way."""
+    from paper_1212_2287_b200.synth import complete_flat
+    monkeypatch.setenv("TS_SK", "1")
+    if ctas:
+        monkeypatch.setenv("TS_SK_CTAS", ctas)
+    rng = np.random.default_rng(len(kind) * 77 + n)
+    T, d, F = 330, 7, 40
+    n_int = (1 << d) - 1
+    flat = complete_flat(F, d, rng.integers(0, F, (T, n_int)), rng.random((T, n_int)),
+                         _leaf_table(kind, rng, T, d))
+    x = rng.random((n, F), dtype=np.float32)
+    s, o = oracle.COracle(flat.arrays()).score(x, threads=4, with_ordinals=True)
+    ev = _ev(flat)
+    assert np.array_equal(ev.predict_batch(x).view(np.uint64), s.view(np.uint64))
+    assert np.array_equal(ev.leaf_indices(x), o.astype(np.int64))
+    ev.close()
+
+
+def test_balanced_tree_split_default_rule():
+    """A batch the planner sends to the balanced split by itself (unit
+    weights, d = 8, tiles filling ~0.3 of the CTA slots): same launches as a
+    forced run, scores and ordinals equal to the oracle's."""
+    from paper_1212_2287_b200 import _lib
+    from paper_1212_2287_b200.synth import complete_flat
+    rng = np.random.default_rng(12)
+    T, d, F, n = 760, 8, 136, 12000
+    n_int = (1 << d) - 1
+    flat = complete_flat(F, d, rng.integers(0, F, (T, n_int)), rng.random((T, n_int)),
+                         rng.standard_normal((T, 1 << d)) * 0.1)
+    x = rng.random((n, F), dtype=np.float32)
+    s, o = oracle.COracle(flat.arrays()).score(x, threads=8, with_ordinals=True)
+    import torch
+    ev = _ev(flat)
+    xd = torch.from_numpy(x).cuda()
+    before = _lib.launch_count()
+    got = ev.score_device(xd).cpu().numpy()
+    assert _lib.launch_count() - before == 2, "expected the walk and k_combine"
+    assert np.array_equal(got.view(np.uint64), s.view(np.uint64))
+    assert np.array_equal(ev.predict_batch(x).view(np.uint64), s.view(np.uint64))
+    assert np.array_equal(ev.leaf_indices(x), o.astype(np.int64))
+    ev.close()
+
+
+@pytest.mark.parametrize("n", [200, 6000])
+def test_balanced_tree_split_weighted(n, monkeypatch):
+    """Non-unit weights: no partial sum is provably exact, so every shared
+    tile's rows are added in tree order from the stored ordinals."""
+    from paper_1212_2287_b200.synth import complete_flat
+    monkeypatch.setenv("TS_SK", "1")
+    rng = np.random.default_rng(n)
+    T, d, F = 250, 8, 136
+    n_int = (1 << d) - 1
+    flat = complete_flat(F, d, rng.integers(0, F, (T, n_int)), rng.random((T, n_int)),
+                         rng.standard_normal((T, 1 << d)), weights=rng.uniform(0.5, 1.5, T))
+    x = rng.random((n, F), dtype=np.float32)
+    s, o = oracle.COracle(flat.arrays()).score(x, threads=4, with_ordinals=True)
+    ev = _ev(flat)
+    assert np.array_equal(ev.predict_batch(x).view(np.uint64), s.view(np.uint64))
+    assert np.array_equal(ev.leaf_indices(x), o.astype(np.int64))
+    ev.close()
+
+
+@pytest.mark.parametrize("d,T,n", [(3, 700, 2000), (10, 60, 3000), (11, 40, 1500), (12, 24, 700)])
+def test_balanced_tree_split_depths(d, T, n, monkeypatch):
+    """Balanced split on the 256-row CTA shape (d >= 10), the global-leaf
+    depths (d >= 11) and shallow trees, with a running sum from a first
+    segment of another depth."""
+    from paper_1212_2287_b200 import Ensemble
+    monkeypatch.setenv("TS_SK", "1")
+    monkeypatch.setenv("TS_RANK", "0")
+    rng = np.random.default_rng(d * 100 + T)
+    f = 24
+    trees = [(_rand_complete(rng, 5, f), 1.0) for _ in range(40)]
+    trees += [(_rand_complete(rng, d, f), 1.0) for _ in range(T)]
+    ens = Ensemble(f, trees)
+    X = rng.random((n, f), dtype=np.float32)
+    s, o = oracle.COracle(ens.flat().arrays()).score(X, threads=4, with_ordinals=True)
+    ev = _ev(ens)
+    assert np.array_equal(ev.predict_batch(X).view(np.uint64), s.view(np.uint64))
+    assert np.array_equal(ev.leaf_indices(X), o.astype(np.int64))
+    ev.close()
+
+
 def test_tree_split_fold_continues_running_sum(monkeypatch):
     """Unit-weight segments of different depths: the second segment's fold
     starts from the first one's sums (acc0 != 0 in the exactness test), also
