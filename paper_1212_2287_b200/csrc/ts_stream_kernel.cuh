@@ -157,7 +157,9 @@ __device__ __forceinline__ void pipe_signal(uint32_t *flag, uint32_t epoch) {
 }
 
 // Transposing stage of B rows into xs[f * B + r] (consumer threads only).
-template <int B>
+// DEEP: also compile the tree-split modes' 12-wide path (kept out of the plain
+// kernels: its 48 live registers change their allocation, +2-3 % at d = 4-10).
+template <int B, bool DEEP = false>
 __device__ __forceinline__ void stage_rows(const StreamArgs &a, float *xs, long long row0) {
     constexpr int kB = B;
     const int r = threadIdx.x;
@@ -169,7 +171,7 @@ __device__ __forceinline__ void stage_rows(const StreamArgs &a, float *xs, long 
     if (((F & 3) == 0) && ((a.ld & 3) == 0) && ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0)) {
         const float4 *x4 = reinterpret_cast<const float4 *>(xrow);
         int c = 0;
-        if (a.splits > 1 || a.sk_ctas > 0) {
+        if (DEEP && (a.splits > 1 || a.sk_ctas > 0)) {
             // tree-split CTAs walk a few trees each, so the staging round
             // trips are their critical path: 12 float4 in flight per thread
             // (a 136-feature row in 3 trips instead of 9)
@@ -529,13 +531,28 @@ __global__ void __launch_bounds__(Shape<CW>::kThreads, Shape<CW>::kCtasPerSm)
         long long tile, pos, end;
         int cb, ce;
     };
+    // (the split modes run on the ORD != 0 instantiations only)
+    constexpr bool kSplitModes = ORD != 0;
+    // The plain kernels keep the loop form they were tuned with (run-time
+    // start / step / chunk range, the uniform split folded in): ptxas's
+    // register allocation of the walk follows it, and the simpler constant
+    // form measured -1 % at d = 4 but +2 % at d = 3 and +3.5 % at d = 10.
+    long long tile0 = blockIdx.x, tstep = gridDim.x;
+    int cb0 = 0, ce0 = nchunks;
+    if (!kSplitModes && a.splits > 1) {
+        tile0 = blockIdx.x % ntiles;
+        tstep = ntiles;
+        const long long j = blockIdx.x / ntiles;
+        cb0 = (int)(j * nchunks / a.splits);
+        ce0 = (int)((j + 1) * nchunks / a.splits);
+    }
     auto span_load = [&](Span &sp) -> bool {
         if (sp.pos >= sp.end) return false;
-        if (a.sk_ctas > 0) {
+        if (kSplitModes && a.sk_ctas > 0) {
             sp.tile = sp.pos / nchunks;
             sp.cb = (int)(sp.pos - sp.tile * nchunks);
             sp.ce = (int)min((long long)nchunks, sp.cb + (sp.end - sp.pos));
-        } else if (a.splits > 1) {
+        } else if (kSplitModes && a.splits > 1) {
             sp.tile = blockIdx.x % ntiles;
             const long long j = blockIdx.x / ntiles;
             sp.cb = (int)(j * nchunks / a.splits);
@@ -548,11 +565,11 @@ __global__ void __launch_bounds__(Shape<CW>::kThreads, Shape<CW>::kCtasPerSm)
         return true;
     };
     auto span_first = [&](Span &sp) -> bool {
-        if (a.sk_ctas > 0) {
+        if (kSplitModes && a.sk_ctas > 0) {
             const long long W = ntiles * nchunks;
             sp.pos = (long long)blockIdx.x * W / a.sk_ctas;
             sp.end = (long long)(blockIdx.x + 1) * W / a.sk_ctas;
-        } else if (a.splits > 1) {
+        } else if (kSplitModes && a.splits > 1) {
             sp.pos = 0;
             sp.end = 1;
         } else {
@@ -562,7 +579,8 @@ __global__ void __launch_bounds__(Shape<CW>::kThreads, Shape<CW>::kCtasPerSm)
         return span_load(sp);
     };
     auto span_next = [&](Span &sp) -> bool {
-        sp.pos += a.sk_ctas > 0 ? (long long)(sp.ce - sp.cb) : a.splits > 1 ? 1 : (long long)gridDim.x;
+        sp.pos += (kSplitModes && a.sk_ctas > 0) ? (long long)(sp.ce - sp.cb)
+                  : (kSplitModes && a.splits > 1) ? 1 : (long long)gridDim.x;
         return span_load(sp);
     };
 
@@ -571,9 +589,8 @@ __global__ void __launch_bounds__(Shape<CW>::kThreads, Shape<CW>::kCtasPerSm)
             // ring position tracked incrementally (no runtime division)
             int s = 0;
             uint32_t ph = 0, used = 0;  // phase of stage s's next reuse; first lap done?
-            Span sp;
-            for (bool more = span_first(sp); more; more = span_next(sp)) {
-                for (int c = sp.cb; c < sp.ce; c++) {
+            auto produce = [&](int cb, int ce) {
+                for (int c = cb; c < ce; c++) {
                     if (used) mbar_wait(empty + s, ph);
                     const int trees = min(a.tpc, a.t1 - a.t0 - c * a.tpc);
                     produce_chunk<D, FW>(a, ring + s * a.chunk_cap, full + s, c, trees);
@@ -583,6 +600,12 @@ __global__ void __launch_bounds__(Shape<CW>::kThreads, Shape<CW>::kCtasPerSm)
                         used = 1;
                     }
                 }
+            };
+            if constexpr (kSplitModes) {
+                Span sp;
+                for (bool more = span_first(sp); more; more = span_next(sp)) produce(sp.cb, sp.ce);
+            } else {
+                for (long long tile = tile0; tile < ntiles; tile += tstep) produce(cb0, ce0);
             }
         }
         return;
@@ -593,17 +616,14 @@ __global__ void __launch_bounds__(Shape<CW>::kThreads, Shape<CW>::kCtasPerSm)
     const uint32_t xr = su32(xs) + 4u * r;
     int s = 0;
     uint32_t ph = 0;  // parity of stage s's current fill
-    Span sp;
-    for (bool more = span_first(sp); more; more = span_next(sp)) {
-        const long long tile = sp.tile;
-        const int cb = sp.cb, ce = sp.ce;
+    auto consume = [&](const long long tile, const int cb, const int ce) {
         const long long row = tile * kB + r;
         const bool valid = row < a.n;
         consumer_sync<kB>();  // previous tile's walks are done with xs
-        stage_rows<kB>(a, xs, tile * kB);
+        stage_rows<kB, ORD != 0>(a, xs, tile * kB);
         consumer_sync<kB>();
         // balanced mode: a tile walked only in part contributes a partial sum from 0
-        const bool part = a.sk_ctas > 0 && (cb != 0 || ce != nchunks);
+        const bool part = kSplitModes && a.sk_ctas > 0 && (cb != 0 || ce != nchunks);
         double acc = (a.accumulate && valid && !part) ? a.out[row] : 0.0;
         LeafPend<K> pend;  // global-leaf depths: the last group's leaves, added late
         // Cross-GPU running-sum pipeline (ts_score_pipe): this warp's 32-row
@@ -662,6 +682,12 @@ __global__ void __launch_bounds__(Shape<CW>::kThreads, Shape<CW>::kCtasPerSm)
         } else if (valid && a.out) {
             a.out[row] = acc;
         }
+    };
+    if constexpr (kSplitModes) {
+        Span sp;
+        for (bool more = span_first(sp); more; more = span_next(sp)) consume(sp.tile, sp.cb, sp.ce);
+    } else {
+        for (long long tile = tile0; tile < ntiles; tile += tstep) consume(tile, cb0, ce0);
     }
 }
 
