@@ -28,3 +28,6 @@ fi
 tail -n 1 "$out/bench.log" | cut -c 1-400
 tail -n 1 "$out/bench_reference.log" | cut -c 1-300
 tail -n 2 "$out/pytest_gpu.log"
+if [ "${CONFIGS:-0}" = 1 ]; then
+    run configs 900 python tools/bench_configs.py --out "$out/configs.jsonl"
+fi
