@@ -293,8 +293,8 @@ struct StreamArgs {
     // one per CTA.  A tile walked by ONE CTA is finished by it; a tile shared
     // by several gets one partial per CTA (part_sum / part_key indexed
     // [tile][slice][row in tile], sk_slices slots per tile) and k_combine
-    // adds them when split_sum_exact allows, else adds the row's leaves in
-    // tree order from the ordinals the walk stored (ord is always set here).
+    // adds them when split_sum_exact allows, else walks the row's trees
+    // again in the blob and adds the leaves in tree order.
     int sk_ctas, sk_slices;
     uint32_t lb_bytes;  // warp-split kernel (k_stream_ws): two tpc x 32 fp32 leaf buffers
     int ws_ctas;        // warp-split kernel: CTAs per SM (2 or 3)

@@ -280,28 +280,62 @@ __global__ void __launch_bounds__(256) k_fold(const double *terms, long long T, 
     }
     if (threadIdx.x < 32 && row < n) out[row] = acc;
 }
+// One tree of a kSplit record (ts_internal.h) walked in global memory for one
+// row: the predicate of ts_stream_kernel.cuh walk_group, the reference's
+// i = (i << 1) + 1 + (x[fid[i]] >= theta[i]) (ref evaluators.py:90-99).
+// Returns the leaf value.
+struct SplitWalk {
+    int D, fw, header;
+    uint32_t thr0, fid0, leaf0, tree_bytes;
+};
+__device__ __forceinline__ float split_walk_global(const unsigned char *tree, const SplitWalk &g,
+                                                   const float *xrow) {
+    const int S = g.D < kTopLevels ? g.D : kTopLevels;
+    uint32_t j = 0;  // 0-based heap index
+    int l = 0;
+    if (g.header) {
+        const uint4 hd = __ldg(reinterpret_cast<const uint4 *>(tree));
+        const bool c0 = __ldg(xrow + (hd.x & 0xffu)) >= __uint_as_float(hd.y);
+        const uint32_t f1 = (hd.x >> (c0 ? 16 : 8)) & 0xffu;
+        const bool c1 = __ldg(xrow + f1) >= __uint_as_float(c0 ? hd.w : hd.z);
+        j = 3u + (c0 ? 2u : 0u) + (c1 ? 1u : 0u);
+        l = 2;
+    }
+    for (; l < S; l++) {
+        const uint2 q = __ldg(reinterpret_cast<const uint2 *>(tree) + j);
+        j = 2u * j + 1u + (__ldg(xrow + (q.x >> kFidShift)) >= __uint_as_float(q.y) ? 1u : 0u);
+    }
+    for (; l < g.D; l++) {
+        const uint32_t k = j + 1u - (1u << S);  // index in the deep arrays
+        const float th = __ldg(reinterpret_cast<const float *>(tree + g.thr0) + k);
+        const uint32_t fid = g.fw == 1 ? (uint32_t)__ldg(tree + g.fid0 + k)
+                                       : (uint32_t)__ldg(reinterpret_cast<const uint16_t *>(tree + g.fid0) + k);
+        j = 2u * j + 1u + (__ldg(xrow + fid) >= th ? 1u : 0u);
+    }
+    return __ldg(reinterpret_cast<const float *>(tree + g.leaf0) + (j + 1u - (1u << g.D)));
+}
+
 // Balanced tree split, second kernel: one CTA per tile.  A tile shared by
 // several walking CTAs (StreamArgs::sk_ctas) has one partial per CTA; a row
 // whose partial sums provably cannot round (split_sum_exact) gets their sum,
 // which then IS the tree-order sum.  Any other row (non-unit weights, a wide
-// leaf range) is added up here in tree order from the per-tree leaf ordinals
-// the walk stored (2 bytes per tree and row instead of an 8-byte term): the
-// leaf values come from the model blob (kSplit record: leaves at leaf0 of each
-// tree_bytes record), term = w * leaf rounded to f64, then the add -- the
+// leaf range: ~2e-4 of the rows for N(0,1) leaves at T = 1000) is scored
+// again here, in tree order: warps 1..15 walk its trees in the model blob
+// (split_walk_global, 480 trees at a time), lane 0 of warp 0 adds the
+// previous batch's terms -- term = w * leaf rounded to f64, then the add, the
 // walk's own arithmetic (ref evaluators.py:529-535).
 // kCombineThreads / B threads fetch each row's partials.
 constexpr int kCombineThreads = 512;
-constexpr int kCombineWarps = kCombineThreads / 32;
-constexpr int kCombineStep = 128;  // terms a warp fetches per step of a row's tree-order chain
+constexpr int kCombineBatch = kCombineThreads - 32;  // trees walked per step of the slow path
 __global__ void __launch_bounds__(kCombineThreads)
     k_combine(const double *part_sum, const uint32_t *part_key, int slices, int B,
               long long ntiles, int nchunks, int ctas, long long T, int accumulate, double *out,
-              long long n, const uint16_t *ord, long long ld_ord, const unsigned char *seg,
-              uint32_t tree_bytes, uint32_t leaf0, const double *weight, int no_fast) {
+              long long n, const float *x, long long ld, const unsigned char *seg, SplitWalk g,
+              const double *weight, int no_fast) {
     __shared__ double rs[kCombineThreads];
     __shared__ double rm[kCombineThreads];
     __shared__ uint32_t rk[kCombineThreads];
-    __shared__ double terms[kCombineWarps][kCombineStep];
+    __shared__ double terms[2][kCombineBatch];
     __shared__ int slow_rows[256];
     __shared__ int n_slow;
     const long long tile = blockIdx.x;
@@ -341,43 +375,32 @@ __global__ void __launch_bounds__(kCombineThreads)
         else slow_rows[atomicAdd(&n_slow, 1)] = r;
     }
     __syncthreads();
-    // Rows whose sums could round: one warp per row.  The lanes fetch the
-    // row's leaf values kCombineStep trees at a time (ordinal, then leaf: two
-    // dependent loads, all in flight together) while lane 0 adds the previous
-    // step's terms in tree order.
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    constexpr int U = kCombineStep / 32;
-    for (int i = warp; i < n_slow; i += kCombineWarps) {
+    const int ns = n_slow;
+    for (int i = 0; i < ns; i++) {
         const long long srow = tile * B + slow_rows[i];
-        const uint16_t *o = ord + srow;
-        double acc = accumulate ? out[srow] : 0.0;
-        double nx[U];
-        auto fetch = [&](long long t0) {
-#pragma unroll
-            for (int u = 0; u < U; u++) {
-                const long long t = t0 + u * 32 + lane;
-                nx[u] = 0.0;
-                if (t < T) {
-                    const float lv = __ldg(reinterpret_cast<const float *>(seg + t * tree_bytes + leaf0) +
-                                           __ldg(o + t * ld_ord));
-                    nx[u] = weight ? __dmul_rn(__ldg(weight + t), (double)lv) : (double)lv;
-                }
+        const float *xrow = x + srow * ld;
+        double acc = 0.0;
+        if (threadIdx.x == 0 && accumulate) acc = out[srow];
+        auto walk_batch = [&](long long t0, double *dst) {
+            const long long t = t0 + (threadIdx.x - 32);
+            if (threadIdx.x >= 32 && t < T) {
+                const float lv = split_walk_global(seg + t * g.tree_bytes, g, xrow);
+                dst[threadIdx.x - 32] = weight ? __dmul_rn(__ldg(weight + t), (double)lv) : (double)lv;
             }
         };
-        fetch(0);
-        for (long long t0 = 0; t0 < T; t0 += kCombineStep) {
-#pragma unroll
-            for (int u = 0; u < U; u++) terms[warp][u * 32 + lane] = nx[u];
-            __syncwarp();
-            if (t0 + kCombineStep < T) fetch(t0 + kCombineStep);
-            if (lane == 0) {
-                const int nt = (int)min((long long)kCombineStep, T - t0);
+        walk_batch(0, terms[0]);
+        __syncthreads();
+        int b = 0;
+        for (long long t0 = 0; t0 < T; t0 += kCombineBatch, b ^= 1) {
+            if (t0 + kCombineBatch < T) walk_batch(t0 + kCombineBatch, terms[b ^ 1]);
+            if (threadIdx.x == 0) {
+                const int nt = (int)min((long long)kCombineBatch, T - t0);
 #pragma unroll 8
-                for (int k = 0; k < nt; k++) acc = __dadd_rn(acc, terms[warp][k]);
+                for (int k = 0; k < nt; k++) acc = __dadd_rn(acc, terms[b][k]);
             }
-            __syncwarp();
+            __syncthreads();
         }
-        if (lane == 0) out[srow] = acc;
+        if (threadIdx.x == 0) out[srow] = acc;
     }
 }
 }  // namespace
@@ -385,20 +408,17 @@ __global__ void __launch_bounds__(kCombineThreads)
 // Balanced tree split ("stream-K"): batches of less than a few waves of tiles
 // -- where whole-tile CTAs leave SMs idle or a last partial wave costs a whole
 // one -- are cut into `ctas` equal runs of (tile, chunk) items
-// (StreamArgs::sk_ctas).  Two launches: the walk (which also stores each
-// tree's leaf ordinal, into the caller's buffer or scratch) and k_combine.
+// (StreamArgs::sk_ctas).  Two launches: the walk and k_combine.
 static cudaError_t launch_balanced(int D, const StreamArgs &a, int ctas, long long tiles,
                                    int nchunks, int device, cudaStream_t stream) {
     const int B = 32 * a.cw;
     const int T = a.t1 - a.t0;
     const int slices = (int)((ctas + tiles - 1) / tiles) + 1;
     const size_t psum_bytes = (size_t)tiles * slices * B * sizeof(double);
-    const long long ld_ord = a.ord ? a.ld_ord : ((a.n + 63) & ~63ll);
-    const size_t ord_bytes = a.ord ? 0 : (size_t)T * ld_ord * sizeof(uint16_t);
     cudaMemPool_t pool = scratch_pool(device);
-    if (!pool || ord_bytes > (128u << 20)) return cudaErrorNotSupported;
+    if (!pool) return cudaErrorNotSupported;
     unsigned char *scratch = nullptr;
-    cudaError_t e = cudaMallocFromPoolAsync((void **)&scratch, 2 * psum_bytes + ord_bytes, pool, stream);
+    cudaError_t e = cudaMallocFromPoolAsync((void **)&scratch, 2 * psum_bytes, pool, stream);
     if (e != cudaSuccess) {
         (void)cudaGetLastError();
         return cudaErrorNotSupported;  // the caller goes on to the other kernels
@@ -418,19 +438,22 @@ static cudaError_t launch_balanced(int D, const StreamArgs &a, int ctas, long lo
     w.sk_slices = slices;
     w.part_sum = reinterpret_cast<double *>(scratch);
     w.part_key = reinterpret_cast<uint32_t *>(scratch + psum_bytes);
-    if (!a.ord) {
-        // the walk indexes ordinals by absolute tree number
-        w.ord = reinterpret_cast<uint16_t *>(scratch + 2 * psum_bytes) - (ptrdiff_t)a.t0 * ld_ord;
-        w.ld_ord = ld_ord;
-    }
     e = stream_detail::kStreamTable[D](w, device, stream);
     if (e == cudaSuccess) {
         const char *ff = getenv("TS_FOLD_FAST");
-        const SplitGeom g = split_geom(D, a.fw);
+        const SplitGeom sg = split_geom(D, a.fw);
+        SplitWalk g;
+        g.D = D;
+        g.fw = a.fw;
+        g.header = split_header(D, a.fw) ? 1 : 0;
+        g.thr0 = sg.thr0;
+        g.fid0 = sg.fid0;
+        g.leaf0 = sg.leaf0;
+        g.tree_bytes = sg.bytes;
         k_combine<<<(unsigned)tiles, kCombineThreads, 0, stream>>>(
             w.part_sum, w.part_key, slices, B, tiles, nchunks, ctas, T, a.accumulate, a.out, a.n,
-            w.ord + (ptrdiff_t)a.t0 * w.ld_ord, w.ld_ord, a.blob + a.seg_byte0, g.bytes, g.leaf0,
-            a.unit_w ? nullptr : a.weight + a.t0, ff && atoi(ff) == 0 ? 1 : 0);
+            w.x, a.ld, a.blob + a.seg_byte0, g, a.unit_w ? nullptr : a.weight + a.t0,
+            ff && atoi(ff) == 0 ? 1 : 0);
         count_launch();
         e = cudaGetLastError();
     }
@@ -468,20 +491,30 @@ cudaError_t launch_stream(int D, const StreamArgs &a0, int device, cudaStream_t 
         splits = f <= 0 ? 1 : std::min(f, nchunks);
     }
     // Balanced tree split (launch_balanced) where it measured faster
-    // (profiles/r2_balanced_split.txt, 1000 trees): unit weights, depth 7-9,
-    // a walk long enough to carry the second launch, and tiles filling
-    // between ~0.3 and ~0.7 of the resident CTA slots -- below that the
-    // uniform split / warp-split kernels win, above it one wave of whole
-    // tiles does (d = 8, T = 1000: n = 12k 87 -> 66 us, 16k 105 -> 82, 20k
-    // 124 -> 99; d = 9: 14k 122 -> 88, 22k 152 -> 126; T = 4000: 10k 336 ->
-    // 184).  Depths <= 6 and >= 10 pay more for the per-tree ordinal store
-    // than the balance returns.  TS_SK=1 forces it (any weights, any shape),
-    // TS_SK=0 disables it; TS_SK_CTAS overrides the CTA count (tests, A/B).
+    // (profiles/r2_balanced_split.txt): its time grows linearly with the
+    // batch, ~13 % above the whole-tile kernel's rate at full waves, while
+    // whole tiles cost whole waves -- so it pays while the last wave is
+    // poorly filled.  With fill = tiles / resident CTA slots: a first wave
+    // filled between 0.12 and 0.8 at d = 7-9 (the uniform split and the
+    // warp-split kernel cover only the smallest batches there), between 0.4
+    // and 0.7 at other depths, or a second / third wave filled to at most
+    // 0.6 (d >= 6).
+    // d=8 T=1000: n = 5k 46 -> 34 us, 12k 87 -> 56, 20k 124 -> 81, 40k 166
+    // -> 149, 50k 212 -> 181; d=6: 16k 64 -> 52, 40k 136 -> 112; d=10 (T =
+    // 300): 20k 61 -> 49, 40k 117 -> 83.  Unit weights only (other sums are
+    // never provably exact) and a walk long enough to carry the second
+    // launch.  TS_SK=1 forces it (any weights, any shape), TS_SK=0 disables
+    // it; TS_SK_CTAS overrides the CTA count (tests, A/B).
     {
         const char *ske = getenv("TS_SK");
         const double fill = (double)tiles / resident;
-        bool sk = a.unit_w && long_walk && D >= 7 && D <= 9 && T <= 4096 &&
-                  (long long)T * D >= 6000 && fill >= (D == 7 ? 0.45 : 0.27) && fill <= 0.72 &&
+        const int waves_done = (int)fill;
+        const double frac = fill - waves_done;
+        const bool mid = D >= 7 && D <= 9;
+        const double lo = mid ? 0.12 : 0.4, hi = mid ? 0.80 : 0.70;
+        bool sk = a.unit_w && long_walk && T <= 4096 && (long long)T * D >= 6000 &&
+                  ((waves_done == 0 && frac >= lo && frac <= hi) ||
+                   (waves_done >= 1 && waves_done <= 2 && frac <= 0.6 && D >= 6)) &&
                   !getenv("TS_SPLIT") && !getenv("TS_WS");
         if (ske) sk = atoi(ske) != 0;
         if (sk && !a.pipe.flags_in && !a.pipe.sums_out) {

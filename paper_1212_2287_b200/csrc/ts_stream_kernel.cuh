@@ -366,7 +366,7 @@ __device__ __forceinline__ void flush_leaves(LeafPend<KP> &pend, double &acc, co
 //    order.
 // ORD: 0 scores only; 1 also ordinals (a.ord) and / or the tree split's terms
 // (a.leaf_out), checked at run time; 2 balanced tree split of a unit-weight
-// ensemble (a.ord set, partial-sum bookkeeping, no terms).
+// ensemble without ordinals (partial-sum bookkeeping only).
 template <int D, int NK, int FW, bool UNIT_W, int ORD, int CW, bool TERMS = false, int KP = 1>
 __device__ __forceinline__ void walk_group(uint32_t tree0, uint32_t xr, double &acc,
                                            const StreamArgs &a, int t, long long row,
@@ -469,7 +469,6 @@ __device__ __forceinline__ void walk_group(uint32_t tree0, uint32_t xr, double &
             acc = __dadd_rn(acc, term);
         }
         if constexpr (ORD == 2) {
-            if (valid) a.ord[(long long)(t + k) * a.ld_ord + row] = (uint16_t)(h - (1u << D));
             pend->kmin1 = min(pend->kmin1, (__float_as_uint(lv) & 0x7fffffffu) - 1u);  // zero wraps: ignored
             if constexpr (!kDefer)
                 pend->amax = max(pend->amax, (uint32_t)__double2hiint(acc) & 0x7fffffffu);
@@ -894,7 +893,7 @@ cudaError_t launch_ws_d(const StreamArgs &a, int device, cudaStream_t stream) {
 
 template <int D, int K, int FW, int CW>
 auto pick_kernel_k(const StreamArgs &a) {
-    if (a.sk_ctas > 0 && a.unit_w) return k_stream<D, K, FW, true, 2, CW>;
+    if (a.sk_ctas > 0 && a.unit_w && !a.ord) return k_stream<D, K, FW, true, 2, CW>;
     if (a.ord || a.leaf_out || a.sk_ctas > 0)
         return a.unit_w ? k_stream<D, K, FW, true, 1, CW> : k_stream<D, K, FW, false, 1, CW>;
     return a.unit_w ? k_stream<D, K, FW, true, 0, CW> : k_stream<D, K, FW, false, 0, CW>;

@@ -454,6 +454,33 @@ def test_balanced_tree_split_default_rule():
     ev.close()
 
 
+@pytest.mark.parametrize("d,F", [(1, 40), (2, 40), (4, 40), (5, 136), (6, 40), (8, 136), (9, 40),
+                                 (10, 40), (12, 24)])
+def test_balanced_tree_split_slow_rows(d, F, monkeypatch):
+    """Rows whose sums could round are walked again by k_combine in the model
+    blob (split_walk_global): every record form -- no deep levels (d <= 5),
+    the 16-byte header and its absence (d = 8), global-leaf depths (rows wide
+    enough for 2-byte fids do not fit the streaming kernel's tile) -- with leaf tables that put most rows on that path."""
+    from paper_1212_2287_b200.synth import complete_flat
+    monkeypatch.setenv("TS_SK", "1")
+    monkeypatch.setenv("TS_RANK", "0")
+    rng = np.random.default_rng(d * 1000 + F)
+    T, n = max(24, 600 >> max(0, d - 6)), 700
+    n_int = (1 << d) - 1
+    thetas = rng.random((T, n_int))
+    thetas[rng.random((T, n_int)) < 0.2] = 0.5  # ties with the rows below
+    flat = complete_flat(F, d, rng.integers(0, F, (T, n_int)), thetas,
+                         _leaf_table("wide", rng, T, d))
+    x = rng.random((n, F), dtype=np.float32)
+    x[::7, ::3] = 0.5
+    s, o = oracle.COracle(flat.arrays()).score(x, threads=4, with_ordinals=True)
+    ev = _ev(flat)
+    assert ev.model.info["complete_trees"] == T
+    assert np.array_equal(ev.predict_batch(x).view(np.uint64), s.view(np.uint64))
+    assert np.array_equal(ev.leaf_indices(x), o.astype(np.int64))
+    ev.close()
+
+
 @pytest.mark.parametrize("n", [200, 6000])
 def test_balanced_tree_split_weighted(n, monkeypatch):
     """Non-unit weights: no partial sum is provably exact, so every shared
