@@ -54,6 +54,10 @@ struct Segment {
     int chunk0 = 0, nchunks = 0;  // kCStream: chunk table range
     int cs_b = 0;                 // kCStream: instance tile the records were encoded for
     int rank_space = 0;           // kRank: index into DeviceTables::rank_spaces
+    // kSplit: expected fraction of rows whose tree-order sum may round (pack-
+    // time estimate from the leaf magnitudes, ts_pack.cpp slow_row_rate): the
+    // balanced tree split scores such rows a second time, one after another.
+    float slow_rows = 0.f;
 };
 
 // All trees live in one byte blob, tree t at byte 16 * tree_off16[t]:
@@ -296,6 +300,7 @@ struct StreamArgs {
     // adds them when split_sum_exact allows, else walks the row's trees
     // again in the blob and adds the leaves in tree order.
     int sk_ctas, sk_slices;
+    float slow_rows;  // Segment::slow_rows
     uint32_t lb_bytes;  // warp-split kernel (k_stream_ws): two tpc x 32 fp32 leaf buffers
     int ws_ctas;        // warp-split kernel: CTAs per SM (2 or 3)
     int k;              // k_stream lockstep chains per thread (chains_for_depth / _fallback)

@@ -340,6 +340,7 @@ cudaError_t launch_segment(const Segment &seg, const ScoreArgs &args0, int devic
             sa.F = args.F;
             sa.blob = args.blob;
             sa.seg_byte0 = seg.byte0;
+            sa.slow_rows = seg.slow_rows;
             sa.weight = args.weight;
             sa.t0 = args.t0;
             sa.t1 = args.t1;

@@ -514,6 +514,42 @@ extern "C" int ts_pack_ex(const ts_model_desc *d, int device, int flags, ts_mode
                                       off[t]});
         m->segments.back().rank_space = space;
     }
+    // kSplit segments: how often a row's tree-order sum may round (see
+    // Segment::slow_rows).  The running sums of a row stay below about
+    // M = 4 sqrt(sum_t mean(leaf_t^2)) + sum_t |mean(leaf_t)|; an add is exact
+    // while the leaf's LSB, 2^(e - 23), is no finer than 2^(m - 53) with M <
+    // 2^m, i.e. |leaf| >= 2^(m - 30).  A row meets T leaves, so about
+    // T x (share of nonzero leaves below that) of the rows are not provably
+    // exact -- 2e-4 for N(0,1) leaves at T = 1000, most rows for leaves
+    // spread over many decades.
+    for (Segment &sg : m->segments) {
+        if (sg.layout != kSplit) continue;
+        double sum_ms = 0.0, sum_mean = 0.0;
+        std::vector<double> mags;
+        for (int t = sg.t0; t < sg.t1; t++) {
+            const int64_t o = d->tree_node_offset[t], e = d->tree_node_offset[t + 1];
+            double s1 = 0.0, s2 = 0.0;
+            int64_t nl = 0;
+            for (int64_t i = o; i < e; i++) {
+                if (d->node_fid[i] >= 0) continue;
+                const double v = d->node_value[i];
+                s1 += v;
+                s2 += v * v;
+                nl++;
+                if (v != 0.0) mags.push_back(fabs(v));
+            }
+            if (nl) {
+                sum_ms += s2 / nl;
+                sum_mean += fabs(s1 / nl);
+            }
+        }
+        const double M = 4.0 * sqrt(sum_ms) + sum_mean;
+        if (mags.empty() || !(M > 0.0)) continue;
+        const double thr = ldexp(M, 1 - 30);
+        size_t tiny = 0;
+        for (double v : mags) tiny += v < thr;
+        sg.slow_rows = (float)std::min(1.0, (double)(sg.t1 - sg.t0) * tiny / mags.size());
+    }
     // kCStream chunk tables: consecutive trees up to tpc / chunk_cap bytes;
     // inside a chunk the slots are ordered by depth (deepest first) so the
     // kernel's lockstep K-groups walk trees of nearly equal depth.

@@ -180,7 +180,7 @@ __device__ __forceinline__ void fold_load(double *dst, const double *src, int tr
 // evaluators.py:529-535) equals the plain sum of the splits' own sums.
 // kmin1: smallest nonzero |leaf| bit pattern minus 1 (0xffffffff: no nonzero
 // term).  Otherwise (wide dynamic range; non-unit weights send amax = all
-// ones, i.e. M = NaN) the caller adds the terms one by one in tree order.
+// ones, i.e. M = infinity) the caller adds the terms one by one in tree order.
 __device__ __forceinline__ double amax_bound(uint32_t amax) {
     // >= the |sum| whose high word is amax; all ones (non-unit weights) and
     // anything at the top of the range: infinity, which fails the test
@@ -502,8 +502,10 @@ cudaError_t launch_stream(int D, const StreamArgs &a0, int device, cudaStream_t 
     // d=8 T=1000: n = 5k 46 -> 34 us, 12k 87 -> 56, 20k 124 -> 81, 40k 166
     // -> 149, 50k 212 -> 181; d=6: 16k 64 -> 52, 40k 136 -> 112; d=10 (T =
     // 300): 20k 61 -> 49, 40k 117 -> 83.  Unit weights only (other sums are
-    // never provably exact) and a walk long enough to carry the second
-    // launch.  TS_SK=1 forces it (any weights, any shape), TS_SK=0 disables
+    // never provably exact), leaves whose magnitudes leave at most ~0.1 % of
+    // the rows to k_combine's one-at-a-time second walk (Segment::slow_rows:
+    // 11.6 us per row at T = 1000), and a walk long enough to carry the
+    // second launch.  TS_SK=1 forces it (any weights, any shape), TS_SK=0 disables
     // it; TS_SK_CTAS overrides the CTA count (tests, A/B).
     {
         const char *ske = getenv("TS_SK");
@@ -513,6 +515,7 @@ cudaError_t launch_stream(int D, const StreamArgs &a0, int device, cudaStream_t 
         const bool mid = D >= 7 && D <= 9;
         const double lo = mid ? 0.12 : 0.4, hi = mid ? 0.80 : 0.70;
         bool sk = a.unit_w && long_walk && T <= 4096 && (long long)T * D >= 6000 &&
+                  a.slow_rows <= 1e-3f &&
                   ((waves_done == 0 && frac >= lo && frac <= hi) ||
                    (waves_done >= 1 && waves_done <= 2 && frac <= 0.6 && D >= 6)) &&
                   !getenv("TS_SPLIT") && !getenv("TS_WS");
