@@ -54,7 +54,7 @@ struct Segment {
     int chunk0 = 0, nchunks = 0;  // kCStream: chunk table range
     int cs_b = 0;                 // kCStream: instance tile the records were encoded for
     int rank_space = 0;           // kRank: index into DeviceTables::rank_spaces
-    // kSplit: expected fraction of rows whose tree-order sum may round (pack-
+    // kSplit / kRank: expected fraction of rows whose tree-order sum may round (pack-
     // time estimate from the leaf magnitudes, ts_pack.cpp slow_row_rate): the
     // balanced tree split scores such rows a second time, one after another.
     float slow_rows = 0.f;
@@ -155,6 +155,17 @@ constexpr int kRankMaxU = 0x7ffe;        // distinct thresholds per feature
 constexpr int kRankB = 256;              // rows per rank tile (R layout and kernel)
 constexpr int kRankMaxDepth = 14;        // deepest tree the rank walk streams (d = 13-14:
                                          // the fp32 layouts only have the L1 path there)
+// u16 slot of row r (0..255) in a feature's 512-byte run of a rank tile:
+// warps 2k and 2k+1 share 32-bit words (low / high halves), lane l of a warp
+// in word 32k + l -- so a warp's 32 lanes read 32 distinct banks for any mix
+// of features (two rows of one warp in one word would be a 2-way conflict on
+// every x read).
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+constexpr uint32_t rank_slot(uint32_t r) {
+    return ((((r >> 5) >> 1) << 5) + (r & 31u)) * 2u + ((r >> 5) & 1u);
+}
 struct RankGeom {
     uint32_t leaf0, bytes;
 };
@@ -347,6 +358,25 @@ bool plan_cstream(int F, int device, CStreamArgs *a);
 
 // Rank kernels (ts_rank.cu): whether depth D over F features has a plan on
 // this device, and the launch of one kRank segment (pre-pass + walk).
+// Second kernel of a balanced tree split (ts_stream.cu k_combine): adds the
+// partials of every tile shared by several CTAs, or scores a row again in tree
+// order when its sums could round.  The record form the second walk reads:
+struct LeafWalk {
+    int rank;                 // 0: kSplit record + fp32 rows; 1: kRank record + rank tiles
+    int D, fw, header;        // kSplit: depth, fid width, 16-byte header
+    uint32_t thr0, fid0, leaf0, tree_bytes;
+    const float *x;           // kSplit: rows, stride ld
+    long long ld;
+    const uint16_t *R;        // kRank: [tile][F][256] instance ranks
+    int F;
+    const unsigned char *seg; // first tree of the segment
+    const double *weight;     // nullptr: unit weights
+};
+cudaError_t launch_combine(const double *part_sum, const uint32_t *part_key, int slices, int B,
+                           long long tiles, int nchunks, int ctas, long long T, int accumulate,
+                           double *out, long long n, const LeafWalk &walk, cudaStream_t stream);
+// The planner's test for the balanced split (fill of the last wave of tiles).
+bool balanced_split_pays(int D, long long T, long long tiles, int resident, bool has_small_batch_paths);
 bool rank_plan_ok(int F, int D, int device);
 cudaError_t launch_rank_segment(const Segment &seg, const ScoreArgs &args, int device,
                                 cudaStream_t stream);

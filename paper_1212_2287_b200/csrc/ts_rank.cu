@@ -264,7 +264,54 @@ cudaError_t rank_chunk(const Segment &seg, const ScoreArgs &args, int device,
         a.out = args.out;
         a.ord = args.ord;
         a.ld_ord = args.ld_ord;
+        // Balanced tree split (ts_stream.cu launch_balanced; the rank walk has
+        // no other small-batch path: a 256-row tile is walked by one CTA over
+        // all trees, so d=12 T=1000 cost ~250 us for ANY batch up to 30k
+        // rows).  Unit weights, no ordinals, few rows whose sums may round.
+        const int sms = dev_attrs(device).sms;
+        const int T = args.t1 - args.t0;
+        const int nchunks = (T + a.tpc - 1) / a.tpc;
+        const char *ske = getenv("TS_SK");
+        bool sk = args.unit_w && !args.ord && seg.slow_rows <= 1e-3f &&
+                  balanced_split_pays(seg.depth, T, tiles, sms, false);
+        if (ske) sk = atoi(ske) != 0 && args.unit_w && !args.ord;
+        const long long W = tiles * nchunks;
+        long long ctas = std::min<long long>(sms, W);
+        if (const char *ce = getenv("TS_SK_CTAS")) ctas = std::min<long long>(std::max(1, atoi(ce)), W);
+        unsigned char *scratch = nullptr;
+        size_t psum_bytes = 0;
+        int slices = 0;
+        if (sk && (ctas > tiles || tiles % ctas != 0)) {
+            slices = (int)((ctas + tiles - 1) / tiles) + 1;
+            psum_bytes = (size_t)tiles * slices * kRankB * sizeof(double);
+            if (cudaMallocFromPoolAsync((void **)&scratch, 2 * psum_bytes, pool, stream) != cudaSuccess) {
+                (void)cudaGetLastError();
+                scratch = nullptr;  // whole tiles instead
+            }
+        }
+        if (scratch) {
+            a.sk_ctas = (int)ctas;
+            a.sk_slices = slices;
+            a.part_sum = reinterpret_cast<double *>(scratch);
+            a.part_key = reinterpret_cast<uint32_t *>(scratch + psum_bytes);
+        }
         e = kRankTable[seg.depth](a, K, device, stream);
+        if (scratch) {
+            if (e == cudaSuccess) {
+                LeafWalk g{};
+                g.rank = 1;
+                g.D = seg.depth;
+                g.leaf0 = a.leaf0;
+                g.tree_bytes = a.tree_bytes;
+                g.R = R;
+                g.F = args.F;
+                g.seg = args.blob + seg.byte0;
+                e = launch_combine(a.part_sum, a.part_key, slices, kRankB, tiles, nchunks, (int)ctas,
+                                   T, args.accumulate, args.out, args.n, g, stream);
+            }
+            const cudaError_t f2 = cudaFreeAsync(scratch, stream);
+            if (e == cudaSuccess) e = f2;
+        }
     }
     const cudaError_t f = cudaFreeAsync(R, stream);
     return e != cudaSuccess ? e : f;

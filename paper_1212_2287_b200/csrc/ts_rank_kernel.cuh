@@ -37,14 +37,7 @@ namespace rank_detail {
 using namespace stream_detail;
 
 constexpr int kCW = 8;                  // consumer warps: 256-row tiles
-// u16 slot of row r (0..255) in a feature's 512-byte run of a rank tile:
-// warps 2k and 2k+1 share 32-bit words (low / high halves), lane l of a warp
-// in word 32k + l -- so a warp's 32 lanes read 32 distinct banks for any mix
-// of features (two rows of one warp in one word would be a 2-way conflict on
-// every x read).
-__host__ __device__ constexpr uint32_t rank_slot(uint32_t r) {
-    return ((((r >> 5) >> 1) << 5) + (r & 31u)) * 2u + ((r >> 5) & 1u);
-}
+// (rank_slot: ts_internal.h)
 constexpr int kThreads = kCW * 32 + 32;
 constexpr int kRankMaxStages = 4;
 
@@ -65,6 +58,12 @@ struct RankArgs {
     double *out;
     uint16_t *ord;
     long long ld_ord;
+    // Balanced tree split (ts_stream.cu launch_balanced, same scheme): sk_ctas
+    // CTAs take equal runs of the tile-major (tile, chunk) items; a tile
+    // shared by several CTAs gets one partial per CTA ([tile][slice][row]).
+    int sk_ctas, sk_slices;
+    double *part_sum;
+    uint32_t *part_key;
 };
 
 // ---------------------------------------------------------------------------
@@ -73,9 +72,12 @@ template <int KP>
 struct RankPend {
     float lv[KP];
     int t = 0, n = 0;
+    // balanced split (StreamArgs::part_key): high word of the largest |running
+    // sum|, smallest nonzero |leaf| bit pattern minus 1
+    uint32_t amax = 0u, kmin1 = 0xffffffffu;
 };
 
-template <bool UNIT_W, int KP>
+template <bool UNIT_W, int KP, bool TRACK = false>
 __device__ __forceinline__ void rank_flush(RankPend<KP> &pend, double &acc, const RankArgs &a) {
 #pragma unroll
     for (int j = 0; j < KP; j++) {
@@ -83,6 +85,8 @@ __device__ __forceinline__ void rank_flush(RankPend<KP> &pend, double &acc, cons
             const double term = UNIT_W ? (double)pend.lv[j]
                                        : __dmul_rn(__ldg(a.weight + pend.t + j), (double)pend.lv[j]);
             acc = __dadd_rn(acc, term);
+            if constexpr (TRACK)
+                pend.amax = max(pend.amax, (uint32_t)__double2hiint(acc) & 0x7fffffffu);
         }
     }
     pend.n = 0;
@@ -102,7 +106,9 @@ __device__ __forceinline__ uint32_t lds16(uint32_t addr) {
 }
 
 // NK trees of one ring stage in lockstep, tree k's records at tree0 + k * TB.
-template <int D, int NK, bool UNIT_W, bool ORD, int KP>
+// ORD: 0 scores, 1 also ordinals, 2 balanced split (unit weights, no
+// ordinals: partial-sum bookkeeping).
+template <int D, int NK, bool UNIT_W, int ORD, int KP>
 __device__ __forceinline__ void rank_group(uint32_t tree0, uint32_t TB, uint32_t xr, double &acc,
                                            const RankArgs &a, int t, long long row, bool valid,
                                            RankPend<KP> &pend) {
@@ -125,7 +131,7 @@ __device__ __forceinline__ void rank_group(uint32_t tree0, uint32_t TB, uint32_t
             p[k] = p[k] + p[k] + (c ? hi[k] : lo[k]);
         }
     }
-    if constexpr (kGLeaf) rank_flush<UNIT_W, KP>(pend, acc, a);  // the previous group's leaves
+    if constexpr (kGLeaf) rank_flush<UNIT_W, KP, ORD == 2>(pend, acc, a);  // the previous group's leaves
 #pragma unroll
     for (int k = 0; k < NK; k++) {
         const uint32_t base = tree0 + k * TB;
@@ -148,8 +154,12 @@ __device__ __forceinline__ void rank_group(uint32_t tree0, uint32_t TB, uint32_t
             const double term =
                 UNIT_W ? (double)lv : __dmul_rn(__ldg(a.weight + t + k), (double)lv);
             acc = __dadd_rn(acc, term);
+            if constexpr (ORD == 2)
+                pend.amax = max(pend.amax, (uint32_t)__double2hiint(acc) & 0x7fffffffu);
         }
-        if constexpr (ORD)
+        if constexpr (ORD == 2)
+            pend.kmin1 = min(pend.kmin1, (__float_as_uint(lv) & 0x7fffffffu) - 1u);  // zero wraps: ignored
+        if constexpr (ORD == 1)
             if (a.ord && valid) a.ord[(long long)(t + k) * a.ld_ord + row] = (uint16_t)leaf;
     }
 }
@@ -168,7 +178,7 @@ __device__ __forceinline__ void produce_rank_chunk(const RankArgs &a, unsigned c
     }
 }
 
-template <int D, int K, bool UNIT_W, bool ORD>
+template <int D, int K, bool UNIT_W, int ORD>
 __global__ void __launch_bounds__(kThreads, 1) k_rstream(RankArgs a) {
     constexpr int kB = kCW * 32;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -189,13 +199,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_rstream(RankArgs a) {
     __syncthreads();
     const long long ntiles = (a.n + kB - 1) / kB;
     const int nchunks = (a.t1 - a.t0 + a.tpc - 1) / a.tpc;
+    // balanced split (ORD == 2): this CTA's run of tile-major (tile, chunk) items
+    long long it_lo = 0, it_hi = 0;
+    if constexpr (ORD == 2) {
+        const long long W = ntiles * nchunks;
+        it_lo = (long long)blockIdx.x * W / a.sk_ctas;
+        it_hi = (long long)(blockIdx.x + 1) * W / a.sk_ctas;
+    }
 
     if (warp == kCW) {  // ---- producer warp
         if (lane == 0) {
             int s = 0;
             uint32_t ph = 0, used = 0;
-            for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-                for (int c = 0; c < nchunks; c++) {
+            auto produce = [&](int cb, int ce) {
+                for (int c = cb; c < ce; c++) {
                     if (used) mbar_wait(empty + s, ph);
                     const int trees = min(a.tpc, a.t1 - a.t0 - c * a.tpc);
                     produce_rank_chunk<D>(a, ring + s * a.chunk_cap, full + s, c, trees);
@@ -205,6 +222,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_rstream(RankArgs a) {
                         used = 1;
                     }
                 }
+            };
+            if constexpr (ORD == 2) {
+                for (long long pos = it_lo; pos < it_hi;) {
+                    const int cb = (int)(pos % nchunks);
+                    const int ce = (int)min((long long)nchunks, cb + (it_hi - pos));
+                    produce(cb, ce);
+                    pos += ce - cb;
+                }
+            } else {
+                for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) produce(0, nchunks);
             }
         }
         return;
@@ -217,7 +244,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_rstream(RankArgs a) {
     const int tile_vec = a.F * kB * 2 / 16;  // 16-byte pieces of a rank tile
     int s = 0;
     uint32_t ph = 0;
-    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    auto consume = [&](const long long tile, const int cb, const int ce) {
         const long long row = tile * kB + r;
         const bool valid = row < a.n;
         consumer_sync<kB>();  // previous tile's walks are done with xs
@@ -227,9 +254,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_rstream(RankArgs a) {
             for (int i = r; i < tile_vec; i += kB) dst[i] = __ldg(src + i);
         }
         consumer_sync<kB>();
-        double acc = (a.accumulate && valid) ? a.out[row] : 0.0;
+        // balanced split: a tile walked only in part contributes a partial sum from 0
+        const bool part = ORD == 2 && (cb != 0 || ce != nchunks);
+        double acc = (a.accumulate && valid && !part) ? a.out[row] : 0.0;
         RankPend<K> pend;
-        for (int c = 0; c < nchunks; c++) {
+        for (int c = cb; c < ce; c++) {
             mbar_wait(full + s, ph);
             const uint32_t buf = su32(ring + s * a.chunk_cap);
             const int t0 = a.t0 + c * a.tpc;
@@ -248,8 +277,30 @@ __global__ void __launch_bounds__(kThreads, 1) k_rstream(RankArgs a) {
                 ph ^= 1u;
             }
         }
-        if constexpr (D >= 11) rank_flush<UNIT_W, K>(pend, acc, a);
-        if (valid && a.out) a.out[row] = acc;
+        if constexpr (D >= 11) rank_flush<UNIT_W, K, ORD == 2>(pend, acc, a);
+        if (part) {
+            if (valid) {  // slice = this CTA's rank among the CTAs sharing the tile
+                const long long W = ntiles * nchunks;
+                const long long b0 = ((tile * nchunks + 1) * a.sk_ctas - 1) / W;
+                const long long pj = (tile * a.sk_slices + (blockIdx.x - b0)) * kB + r;
+                a.part_sum[pj] = acc;
+                a.part_key[2 * pj] = pend.amax;
+                a.part_key[2 * pj + 1] = pend.kmin1;
+            }
+        } else if (valid && a.out) {
+            a.out[row] = acc;
+        }
+    };
+    if constexpr (ORD == 2) {
+        for (long long pos = it_lo; pos < it_hi;) {
+            const long long tile = pos / nchunks;
+            const int cb = (int)(pos - tile * nchunks);
+            const int ce = (int)min((long long)nchunks, cb + (it_hi - pos));
+            consume(tile, cb, ce);
+            pos += ce - cb;
+        }
+    } else {
+        for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) consume(tile, 0, nchunks);
     }
 }
 
@@ -273,8 +324,9 @@ cudaError_t launch_rank_d(const RankArgs &a, int k, int device, cudaStream_t str
     constexpr int K1 = rank_chains(D), K2 = rank_chains_fallback(D);
     auto pick = [&](auto kc) {
         constexpr int KK = decltype(kc)::value;
-        if (a.ord) return a.unit_w ? k_rstream<D, KK, true, true> : k_rstream<D, KK, false, true>;
-        return a.unit_w ? k_rstream<D, KK, true, false> : k_rstream<D, KK, false, false>;
+        if (a.sk_ctas > 0) return k_rstream<D, KK, true, 2>;  // unit weights, no ordinals
+        if (a.ord) return a.unit_w ? k_rstream<D, KK, true, 1> : k_rstream<D, KK, false, 1>;
+        return a.unit_w ? k_rstream<D, KK, true, 0> : k_rstream<D, KK, false, 0>;
     };
     auto kern = k == K1 ? pick(std::integral_constant<int, K1>{})
                         : pick(std::integral_constant<int, K2>{});
@@ -284,7 +336,8 @@ cudaError_t launch_rank_d(const RankArgs &a, int k, int device, cudaStream_t str
     if (e != cudaSuccess) return e;
     const long long tiles = (a.n + kRankB - 1) / kRankB;
     const int sms = dev_attrs(device).sms;
-    kern<<<(int)std::min<long long>(tiles, sms), kThreads, smem, stream>>>(a);
+    const int grid = a.sk_ctas > 0 ? a.sk_ctas : (int)std::min<long long>(tiles, sms);
+    kern<<<grid, kThreads, smem, stream>>>(a);
     count_launch();
     return cudaGetLastError();
 }

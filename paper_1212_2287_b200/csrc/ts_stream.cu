@@ -280,18 +280,29 @@ __global__ void __launch_bounds__(256) k_fold(const double *terms, long long T, 
     }
     if (threadIdx.x < 32 && row < n) out[row] = acc;
 }
-// One tree of a kSplit record (ts_internal.h) walked in global memory for one
-// row: the predicate of ts_stream_kernel.cuh walk_group, the reference's
-// i = (i << 1) + 1 + (x[fid[i]] >= theta[i]) (ref evaluators.py:90-99).
-// Returns the leaf value.
-struct SplitWalk {
-    int D, fw, header;
-    uint32_t thr0, fid0, leaf0, tree_bytes;
-};
-__device__ __forceinline__ float split_walk_global(const unsigned char *tree, const SplitWalk &g,
-                                                   const float *xrow) {
-    const int S = g.D < kTopLevels ? g.D : kTopLevels;
+// One tree walked in global memory for one row, from the segment's packed
+// records (LeafWalk, ts_internal.h) -- the predicate of the streaming walks,
+// the reference's i = (i << 1) + 1 + (x[fid[i]] >= theta[i]) (ref
+// evaluators.py:90-99).  Returns the leaf value.
+//  * kSplit (ts_stream_kernel.cuh walk_group): header / top records / deep
+//    arrays, fp32 thresholds against the row's fp32 values;
+//  * kRank (ts_rank_kernel.cuh rank_group): 4-byte records fid << 24 | rank
+//    against the row's u16 ranks in its rank tile.
+__device__ __forceinline__ float leaf_walk_global(const unsigned char *tree, const LeafWalk &g,
+                                                  long long row) {
     uint32_t j = 0;  // 0-based heap index
+    if (g.rank) {
+        const uint16_t *rr = g.R + (row / kRankB) * g.F * kRankB + rank_slot((uint32_t)(row % kRankB));
+        const uint32_t *recs = reinterpret_cast<const uint32_t *>(tree);
+        for (int l = 0; l < g.D; l++) {
+            const uint32_t rec = __ldg(recs + j);
+            const uint32_t v = __ldg(rr + (rec >> 24) * kRankB);
+            j = 2u * j + 1u + ((v | (rec & 0xff000000u)) >= rec ? 1u : 0u);
+        }
+        return __ldg(reinterpret_cast<const float *>(tree + g.leaf0) + (j + 1u - (1u << g.D)));
+    }
+    const float *xrow = g.x + row * g.ld;
+    const int S = g.D < kTopLevels ? g.D : kTopLevels;
     int l = 0;
     if (g.header) {
         const uint4 hd = __ldg(reinterpret_cast<const uint4 *>(tree));
@@ -321,7 +332,7 @@ __device__ __forceinline__ float split_walk_global(const unsigned char *tree, co
 // which then IS the tree-order sum.  Any other row (non-unit weights, a wide
 // leaf range: ~2e-4 of the rows for N(0,1) leaves at T = 1000) is scored
 // again here, in tree order: warps 1..15 walk its trees in the model blob
-// (split_walk_global, 480 trees at a time), lane 0 of warp 0 adds the
+// (leaf_walk_global, 480 trees at a time), lane 0 of warp 0 adds the
 // previous batch's terms -- term = w * leaf rounded to f64, then the add, the
 // walk's own arithmetic (ref evaluators.py:529-535).
 // kCombineThreads / B threads fetch each row's partials.
@@ -330,8 +341,7 @@ constexpr int kCombineBatch = kCombineThreads - 32;  // trees walked per step of
 __global__ void __launch_bounds__(kCombineThreads)
     k_combine(const double *part_sum, const uint32_t *part_key, int slices, int B,
               long long ntiles, int nchunks, int ctas, long long T, int accumulate, double *out,
-              long long n, const float *x, long long ld, const unsigned char *seg, SplitWalk g,
-              const double *weight, int no_fast) {
+              long long n, LeafWalk g, int no_fast) {
     __shared__ double rs[kCombineThreads];
     __shared__ double rm[kCombineThreads];
     __shared__ uint32_t rk[kCombineThreads];
@@ -378,14 +388,13 @@ __global__ void __launch_bounds__(kCombineThreads)
     const int ns = n_slow;
     for (int i = 0; i < ns; i++) {
         const long long srow = tile * B + slow_rows[i];
-        const float *xrow = x + srow * ld;
         double acc = 0.0;
         if (threadIdx.x == 0 && accumulate) acc = out[srow];
         auto walk_batch = [&](long long t0, double *dst) {
             const long long t = t0 + (threadIdx.x - 32);
             if (threadIdx.x >= 32 && t < T) {
-                const float lv = split_walk_global(seg + t * g.tree_bytes, g, xrow);
-                dst[threadIdx.x - 32] = weight ? __dmul_rn(__ldg(weight + t), (double)lv) : (double)lv;
+                const float lv = leaf_walk_global(g.seg + t * g.tree_bytes, g, srow);
+                dst[threadIdx.x - 32] = g.weight ? __dmul_rn(__ldg(g.weight + t), (double)lv) : (double)lv;
             }
         };
         walk_batch(0, terms[0]);
@@ -404,6 +413,44 @@ __global__ void __launch_bounds__(kCombineThreads)
     }
 }
 }  // namespace
+
+cudaError_t launch_combine(const double *part_sum, const uint32_t *part_key, int slices, int B,
+                           long long tiles, int nchunks, int ctas, long long T, int accumulate,
+                           double *out, long long n, const LeafWalk &walk, cudaStream_t stream) {
+    // TS_FOLD_FAST=0: every shared tile's rows on the tree-order path (tests, A/B)
+    const char *ff = getenv("TS_FOLD_FAST");
+    k_combine<<<(unsigned)tiles, kCombineThreads, 0, stream>>>(
+        part_sum, part_key, slices, B, tiles, nchunks, ctas, T, accumulate, out, n, walk,
+        ff && atoi(ff) == 0 ? 1 : 0);
+    count_launch();
+    return cudaGetLastError();
+}
+
+// Where the balanced split measured faster (profiles/r2_balanced_split.txt):
+// its time grows linearly with the batch, ~13 % above the whole-tile kernel's
+// rate at full waves, while whole tiles cost whole waves -- so it pays while
+// the last wave is poorly filled.  With fill = tiles / resident CTA slots: a
+// first wave filled up to 0.8 at d = 7-9 and 0.7 elsewhere -- from 0.12 (d =
+// 7-9) / 0.4 up where the uniform split and the warp-split kernel serve the
+// smallest batches (has_small_batch_paths), from the first tile where nothing
+// else does (the rank walk) -- or a second / third wave filled to at most 0.6
+// (d >= 6).  The walk must be long enough to carry the second launch.
+bool balanced_split_pays(int D, long long T, long long tiles, int resident,
+                         bool has_small_batch_paths) {
+    if (T > 4096 || T * D < 6000) return false;
+    const double fill = (double)tiles / resident;
+    const int waves_done = (int)fill;
+    const double frac = fill - waves_done;
+    const bool mid = D >= 7 && D <= 9;
+    // (the rank walk's balanced kernel carries no ordinal / split checks of
+    // its own, so it stays ahead up to fuller waves: d=12 T=1000 n = 30k,
+    // fill 0.8: 332 -> 294 us)
+    const double lo = !has_small_batch_paths ? 0.0 : mid ? 0.12 : 0.4;
+    const double hi = !has_small_batch_paths ? 0.90 : mid ? 0.80 : 0.70;
+    const double hi2 = !has_small_batch_paths ? 0.75 : 0.60;
+    return (waves_done == 0 && frac >= lo && frac <= hi) ||
+           (waves_done >= 1 && waves_done <= 2 && frac <= hi2 && D >= 6);
+}
 
 // Balanced tree split ("stream-K"): batches of less than a few waves of tiles
 // -- where whole-tile CTAs leave SMs idle or a last partial wave costs a whole
@@ -440,9 +487,8 @@ static cudaError_t launch_balanced(int D, const StreamArgs &a, int ctas, long lo
     w.part_key = reinterpret_cast<uint32_t *>(scratch + psum_bytes);
     e = stream_detail::kStreamTable[D](w, device, stream);
     if (e == cudaSuccess) {
-        const char *ff = getenv("TS_FOLD_FAST");
         const SplitGeom sg = split_geom(D, a.fw);
-        SplitWalk g;
+        LeafWalk g{};
         g.D = D;
         g.fw = a.fw;
         g.header = split_header(D, a.fw) ? 1 : 0;
@@ -450,12 +496,12 @@ static cudaError_t launch_balanced(int D, const StreamArgs &a, int ctas, long lo
         g.fid0 = sg.fid0;
         g.leaf0 = sg.leaf0;
         g.tree_bytes = sg.bytes;
-        k_combine<<<(unsigned)tiles, kCombineThreads, 0, stream>>>(
-            w.part_sum, w.part_key, slices, B, tiles, nchunks, ctas, T, a.accumulate, a.out, a.n,
-            w.x, a.ld, a.blob + a.seg_byte0, g, a.unit_w ? nullptr : a.weight + a.t0,
-            ff && atoi(ff) == 0 ? 1 : 0);
-        count_launch();
-        e = cudaGetLastError();
+        g.x = w.x;
+        g.ld = a.ld;
+        g.seg = a.blob + a.seg_byte0;
+        g.weight = a.unit_w ? nullptr : a.weight + a.t0;
+        e = launch_combine(w.part_sum, w.part_key, slices, B, tiles, nchunks, ctas, T, a.accumulate,
+                           a.out, a.n, g, stream);
     }
     cudaError_t f = cudaFreeAsync(scratch, stream);
     if (xcopy) {
@@ -491,34 +537,19 @@ cudaError_t launch_stream(int D, const StreamArgs &a0, int device, cudaStream_t 
         splits = f <= 0 ? 1 : std::min(f, nchunks);
     }
     // Balanced tree split (launch_balanced) where it measured faster
-    // (profiles/r2_balanced_split.txt): its time grows linearly with the
-    // batch, ~13 % above the whole-tile kernel's rate at full waves, while
-    // whole tiles cost whole waves -- so it pays while the last wave is
-    // poorly filled.  With fill = tiles / resident CTA slots: a first wave
-    // filled between 0.12 and 0.8 at d = 7-9 (the uniform split and the
-    // warp-split kernel cover only the smallest batches there), between 0.4
-    // and 0.7 at other depths, or a second / third wave filled to at most
-    // 0.6 (d >= 6).
-    // d=8 T=1000: n = 5k 46 -> 34 us, 12k 87 -> 56, 20k 124 -> 81, 40k 166
-    // -> 149, 50k 212 -> 181; d=6: 16k 64 -> 52, 40k 136 -> 112; d=10 (T =
-    // 300): 20k 61 -> 49, 40k 117 -> 83.  Unit weights only (other sums are
-    // never provably exact), leaves whose magnitudes leave at most ~0.1 % of
-    // the rows to k_combine's one-at-a-time second walk (Segment::slow_rows:
-    // 11.6 us per row at T = 1000), and a walk long enough to carry the
-    // second launch.  TS_SK=1 forces it (any weights, any shape), TS_SK=0 disables
-    // it; TS_SK_CTAS overrides the CTA count (tests, A/B).
+    // (balanced_split_pays): d=8 T=1000: n = 5k 46 -> 34 us, 12k 87 -> 56,
+    // 20k 124 -> 81, 40k 166 -> 149, 50k 212 -> 181; d=6: 16k 64 -> 52, 40k
+    // 136 -> 112; d=10 (T = 300): 20k 61 -> 49, 40k 117 -> 83.  Unit weights
+    // only (other sums are never provably exact) and leaves whose magnitudes
+    // leave at most ~0.1 % of the rows to k_combine's one-at-a-time second
+    // walk (Segment::slow_rows: 11.6 us per row at T = 1000).  TS_SK=1
+    // forces it (any weights, any shape), TS_SK=0 disables it; TS_SK_CTAS
+    // overrides the CTA count (tests, A/B).
     {
         const char *ske = getenv("TS_SK");
-        const double fill = (double)tiles / resident;
-        const int waves_done = (int)fill;
-        const double frac = fill - waves_done;
-        const bool mid = D >= 7 && D <= 9;
-        const double lo = mid ? 0.12 : 0.4, hi = mid ? 0.80 : 0.70;
-        bool sk = a.unit_w && long_walk && T <= 4096 && (long long)T * D >= 6000 &&
-                  a.slow_rows <= 1e-3f &&
-                  ((waves_done == 0 && frac >= lo && frac <= hi) ||
-                   (waves_done >= 1 && waves_done <= 2 && frac <= 0.6 && D >= 6)) &&
-                  !getenv("TS_SPLIT") && !getenv("TS_WS");
+        bool sk = a.unit_w && long_walk && a.slow_rows <= 1e-3f &&
+                  balanced_split_pays(D, T, tiles, resident, true) && !getenv("TS_SPLIT") &&
+                  !getenv("TS_WS");
         if (ske) sk = atoi(ske) != 0;
         if (sk && !a.pipe.flags_in && !a.pipe.sums_out) {
             const long long W = tiles * nchunks;

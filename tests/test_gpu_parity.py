@@ -1148,6 +1148,54 @@ def test_rank_layout_forced_all_depths(depth, ties, monkeypatch):
     assert np.array_equal(ev.score_device(torch.from_numpy(X).cuda()).cpu().numpy(), s)
 
 
+@pytest.mark.parametrize("depth", [2, 7, 10, 12, 13])
+@pytest.mark.parametrize("kind", ["narrow", "wide", "zeros"])
+@pytest.mark.parametrize("n,ctas", [(1, None), (700, None), (700, "5"), (5000, "37")])
+def test_rank_layout_balanced_split(depth, kind, n, ctas, monkeypatch):
+    """Balanced tree split on the rank walk (k_rstream<..., ORD = 2>, the
+    same k_combine): tiles shared by several CTAs combined from their partial
+    sums when provably exact, else walked again from the rank records and the
+    row's rank tile; unit weights, scores against the oracle bit for bit, also
+    continuing the running sum of a first segment."""
+    import torch
+    from paper_1212_2287_b200.synth import complete_flat
+    monkeypatch.setenv("TS_RANK_MIN_DEPTH", "1")
+    monkeypatch.setenv("TS_SK", "1")
+    if ctas:
+        monkeypatch.setenv("TS_SK_CTAS", ctas)
+    rng = np.random.default_rng(depth * 131 + n + len(kind))
+    F = 40
+    T = max(12, 400 >> max(0, depth - 6))
+    n_int = (1 << depth) - 1
+    thr = rng.random((T, n_int))
+    thr[rng.random((T, n_int)) < 0.1] = 0.5
+    flat = complete_flat(F, depth, rng.integers(0, F, (T, n_int)), thr,
+                         _leaf_table(kind, rng, T, depth))
+    X = rng.random((n, F), dtype=np.float32)
+    X[::5, ::3] = 0.5
+    s, o = oracle.COracle(flat.arrays()).score(X, threads=4, with_ordinals=True)
+    ev = _ev(flat)
+    assert ev.model.info["rank_trees"] == T
+    assert np.array_equal(ev.predict_batch(X).view(np.uint64), s.view(np.uint64))
+    xd = torch.from_numpy(X).cuda()
+    out = torch.full((n,), 0.375, dtype=torch.float64, device="cuda")
+    ev.model.score(xd, out=out, accumulate=True)   # continues a running sum
+    assert np.array_equal(ev.leaf_indices(X), o.astype(np.int64))
+    # tree-order sum started from 0.375: redo on the host in f64, tree by tree
+    leaves = flat.value.astype(np.float64)
+    exp = np.full(n, 0.375)
+    for t in range(T):
+        base = int(flat.tree_off[t])
+        node = np.zeros(n, np.int64)
+        for _ in range(depth):
+            f = flat.fid[base + node]
+            go = X[np.arange(n), f] >= flat.value[base + node]
+            node = np.where(go, flat.right[base + node], flat.left[base + node])
+        exp = exp + leaves[base + node]
+    assert np.array_equal(out.cpu().numpy().view(np.uint64), exp.view(np.uint64))
+    ev.close()
+
+
 def test_rank_layout_default_choice_and_opt_out(monkeypatch):
     """By default a depth takes the rank layout only with enough trees for
     the walk's savings to pay for the instance-rank pre-pass (ts_pack.cpp
