@@ -120,7 +120,11 @@ __device__ __forceinline__ void walk_loads(uint2 &q, float &v, uint32_t p, uint3
         : "r"(p), "r"(leafmark), "r"(xr));
 }
 
-template <int kK, int G, int W, bool UNIT_W, bool ORD>
+// SK: balanced tree split (CStreamArgs::sk_ctas; unit weights, no ordinals):
+// the CTA walks a run of (tile, chunk) items; the accumulator warp also keeps
+// the bookkeeping of ts_stream.cu split_sum_exact and stores a partial for a
+// tile it walked only in part.
+template <int kK, int G, int W, bool UNIT_W, bool ORD, bool SK = false>
 __global__ void __launch_bounds__(threads_c(W), 1) k_cstream(CStreamArgs a) {
     // G (instance groups of 32, B = 32 * G) is a template parameter so the
     // accumulator's per-lane instance loop is fully unrolled with exactly G
@@ -152,13 +156,49 @@ __global__ void __launch_bounds__(threads_c(W), 1) k_cstream(CStreamArgs a) {
     constexpr int B = 32 * G;
     const long long ntiles = (a.n + B - 1) / B;
     const uint32_t lb_half = a.lb_bytes / 2;
+    // Spans (a tile and the chunk range [cb, ce) walked of it) of this CTA:
+    // tiles blockIdx.x, +gridDim.x, ... whole, or (SK) an equal run of the
+    // tile-major (tile, chunk) items.  Every role iterates the same spans.
+    struct Span {
+        long long tile, pos, end;
+        int cb, ce;
+    };
+    auto span_load = [&](Span &sp) -> bool {
+        if (sp.pos >= sp.end) return false;
+        if (SK) {
+            sp.tile = sp.pos / a.nchunks;
+            sp.cb = (int)(sp.pos - sp.tile * a.nchunks);
+            sp.ce = (int)min((long long)a.nchunks, sp.cb + (sp.end - sp.pos));
+        } else {
+            sp.tile = sp.pos;
+            sp.cb = 0;
+            sp.ce = a.nchunks;
+        }
+        return true;
+    };
+    auto span_first = [&](Span &sp) -> bool {
+        if (SK) {
+            const long long Wk = ntiles * a.nchunks;
+            sp.pos = (long long)blockIdx.x * Wk / a.sk_ctas;
+            sp.end = (long long)(blockIdx.x + 1) * Wk / a.sk_ctas;
+        } else {
+            sp.pos = blockIdx.x;
+            sp.end = ntiles;
+        }
+        return span_load(sp);
+    };
+    auto span_next = [&](Span &sp) -> bool {
+        sp.pos += SK ? (long long)(sp.ce - sp.cb) : (long long)gridDim.x;
+        return span_load(sp);
+    };
 
     if (warp == W + 1) {  // ---- producer: TMA bulk copies per chunk
         if (lane == 0) {
             int s = 0;
             uint32_t ph = 0, used = 0;  // phase of stage s's next reuse; first lap done?
-            for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-                for (int c = 0; c < a.nchunks; c++) {
+            Span sp;
+            for (bool more = span_first(sp); more; more = span_next(sp)) {
+                for (int c = sp.cb; c < sp.ce; c++) {
                     if (used) mbar_wait(empty + s, ph);
                     const uint4 ci = __ldg(a.chunk_info + a.chunk0 + c);
                     unsigned char *stage = ring + s * a.stage_bytes;
@@ -180,15 +220,22 @@ __global__ void __launch_bounds__(threads_c(W), 1) k_cstream(CStreamArgs a) {
 
     if (warp == W) {  // ---- accumulator: folds leaves in TREE order
         uint32_t it = 0;
-        for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        Span sp;
+        for (bool more = span_first(sp); more; more = span_next(sp)) {
+            const long long tile = sp.tile;
             const long long row0 = tile * B;
+            // SK: a tile walked only in part contributes a partial sum from 0
+            const bool part = SK && (sp.cb != 0 || sp.ce != a.nchunks);
             double acc[G];
+            uint32_t amax[G], kmin1[G];
 #pragma unroll
             for (int g = 0; g < G; g++) {
                 const long long row = row0 + g * 32 + lane;
-                acc[g] = (a.accumulate && row < a.n) ? a.out[row] : 0.0;
+                acc[g] = (a.accumulate && row < a.n && !part) ? a.out[row] : 0.0;
+                amax[g] = 0u;
+                kmin1[g] = 0xffffffffu;
             }
-            for (int c = 0; c < a.nchunks; c++, it++) {
+            for (int c = sp.cb; c < sp.ce; c++, it++) {
                 const uint4 ci = __ldg(a.chunk_info + a.chunk0 + c);
                 const int nt = (int)ci.z;
                 const int b = it & 1;
@@ -200,17 +247,36 @@ __global__ void __launch_bounds__(threads_c(W), 1) k_cstream(CStreamArgs a) {
                     if constexpr (!UNIT_W) w = __ldg(a.weight + ci.w + i);
 #pragma unroll
                     for (int g = 0; g < G; g++) {
-                        const double lv = (double)lbc[i * B + g * 32 + lane];
+                        const float lf = lbc[i * B + g * 32 + lane];
+                        const double lv = (double)lf;
                         acc[g] = UNIT_W ? __dadd_rn(acc[g], lv) : __dadd_rn(acc[g], __dmul_rn(w, lv));
+                        if constexpr (SK) {
+                            kmin1[g] = min(kmin1[g], (__float_as_uint(lf) & 0x7fffffffu) - 1u);
+                            amax[g] = max(amax[g], (uint32_t)__double2hiint(acc[g]) & 0x7fffffffu);
+                        }
                     }
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(lbe + b);
             }
+            long long pj0 = 0;
+            if (part) {  // slice = this CTA's rank among the CTAs sharing the tile
+                const long long Wk = ntiles * a.nchunks;
+                const long long b0 = ((tile * a.nchunks + 1) * a.sk_ctas - 1) / Wk;
+                pj0 = (tile * a.sk_slices + (blockIdx.x - b0)) * B;
+            }
 #pragma unroll
             for (int g = 0; g < G; g++) {
                 const long long row = row0 + g * 32 + lane;
-                if (row < a.n) a.out[row] = acc[g];
+                if (row >= a.n) continue;
+                if (part) {
+                    const long long pj = pj0 + g * 32 + lane;
+                    a.part_sum[pj] = acc[g];
+                    a.part_key[2 * pj] = amax[g];
+                    a.part_key[2 * pj + 1] = kmin1[g];
+                } else {
+                    a.out[row] = acc[g];
+                }
             }
         }
         return;
@@ -233,14 +299,15 @@ __global__ void __launch_bounds__(threads_c(W), 1) k_cstream(CStreamArgs a) {
     int s = 0;
     uint32_t ph = 0;  // parity of stage s's current fill
     uint32_t it = 0;
-    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const long long row0 = tile * B;
+    Span sp;
+    for (bool more = span_first(sp); more; more = span_next(sp)) {
+        const long long row0 = sp.tile * B;
         consumer_sync<kConsumers>();  // all walks of the previous tile are done
         stage_rows_c<kConsumers, B>(a, xs, row0);
         consumer_sync<kConsumers>();
         const long long walk_row = row0 + inst;
         const bool walk_valid = walk_row < a.n;
-        for (int c = 0; c < a.nchunks; c++, it++) {
+        for (int c = sp.cb; c < sp.ce; c++, it++) {
             const int b = it & 1;
             const uint32_t lbase = lbase0 + b * lb_half;
             mbar_wait(full + s, ph);
@@ -343,14 +410,15 @@ inline size_t cstream_smem(const CStreamArgs &a) {
 
 template <int K, int G, int W>
 cudaError_t launch_kgw(const CStreamArgs &a, int device, cudaStream_t stream) {
-    auto kern = a.ord ? (a.unit_w ? k_cstream<K, G, W, true, true> : k_cstream<K, G, W, false, true>)
-                      : (a.unit_w ? k_cstream<K, G, W, true, false> : k_cstream<K, G, W, false, false>);
+    auto kern = a.sk_ctas > 0 ? k_cstream<K, G, W, true, false, true>  // unit weights, no ordinals
+                : a.ord ? (a.unit_w ? k_cstream<K, G, W, true, true> : k_cstream<K, G, W, false, true>)
+                        : (a.unit_w ? k_cstream<K, G, W, true, false> : k_cstream<K, G, W, false, false>);
     const size_t smem = cstream_smem(a);
     cudaError_t e = ensure_smem((const void *)kern, smem);
     if (e != cudaSuccess) return e;
     const long long tiles = (a.n + a.B - 1) / a.B;
     const int sms = dev_attrs(device).sms;
-    const int grid = (int)(tiles < sms ? tiles : sms);
+    const int grid = a.sk_ctas > 0 ? a.sk_ctas : (int)(tiles < sms ? tiles : sms);
     kern<<<grid, threads_c(W), smem, stream>>>(a);
     count_launch();
     return cudaGetLastError();

@@ -54,7 +54,7 @@ struct Segment {
     int chunk0 = 0, nchunks = 0;  // kCStream: chunk table range
     int cs_b = 0;                 // kCStream: instance tile the records were encoded for
     int rank_space = 0;           // kRank: index into DeviceTables::rank_spaces
-    // kSplit / kRank: expected fraction of rows whose tree-order sum may round (pack-
+    // Streaming layouts: expected fraction of rows whose tree-order sum may round (pack-
     // time estimate from the leaf magnitudes, ts_pack.cpp slow_row_rate): the
     // balanced tree split scores such rows a second time, one after another.
     float slow_rows = 0.f;
@@ -353,6 +353,12 @@ struct CStreamArgs {
     uint16_t *ord;
     long long ld_ord;
     int32_t *status;
+    // Balanced tree split (ts_stream.cu launch_balanced, same scheme): sk_ctas
+    // CTAs take equal runs of the tile-major (tile, chunk) items; a tile
+    // shared by several CTAs gets one partial per CTA ([tile][slice][row]).
+    int sk_ctas, sk_slices;
+    double *part_sum;
+    uint32_t *part_key;
 };
 bool plan_cstream(int F, int device, CStreamArgs *a);
 
@@ -362,21 +368,25 @@ bool plan_cstream(int F, int device, CStreamArgs *a);
 // partials of every tile shared by several CTAs, or scores a row again in tree
 // order when its sums could round.  The record form the second walk reads:
 struct LeafWalk {
-    int rank;                 // 0: kSplit record + fp32 rows; 1: kRank record + rank tiles
+    int rank;                 // 0: kSplit record + fp32 rows; 1: kRank record + rank tiles;
+                              // 2: kCStream child-index records + fp32 rows
     int D, fw, header;        // kSplit: depth, fid width, 16-byte header
     uint32_t thr0, fid0, leaf0, tree_bytes;
-    const float *x;           // kSplit: rows, stride ld
+    const float *x;           // kSplit / kCStream: rows, stride ld
     long long ld;
     const uint16_t *R;        // kRank: [tile][F][256] instance ranks
     int F;
-    const unsigned char *seg; // first tree of the segment
+    const unsigned char *seg; // first tree of the segment (kCStream: the blob)
     const double *weight;     // nullptr: unit weights
+    const uint32_t *tree_off16;  // kCStream: tree t of the segment at 16 * tree_off16[t]
+    int xshift;               // kCStream: record x offset = fid << xshift (4 B bytes per feature)
 };
 cudaError_t launch_combine(const double *part_sum, const uint32_t *part_key, int slices, int B,
                            long long tiles, int nchunks, int ctas, long long T, int accumulate,
                            double *out, long long n, const LeafWalk &walk, cudaStream_t stream);
 // The planner's test for the balanced split (fill of the last wave of tiles).
-bool balanced_split_pays(int D, long long T, long long tiles, int resident, bool has_small_batch_paths);
+bool balanced_split_pays(int D, long long T, long long tiles, int resident, bool has_small_batch_paths,
+                         long long max_trees = 4096);
 bool rank_plan_ok(int F, int D, int device);
 cudaError_t launch_rank_segment(const Segment &seg, const ScoreArgs &args, int device,
                                 cudaStream_t stream);

@@ -329,7 +329,57 @@ cudaError_t launch_segment(const Segment &seg, const ScoreArgs &args0, int devic
         ca.ord = args.ord;
         ca.ld_ord = args.ld_ord;
         ca.status = args.status;
-        return launch_cstream(ca, device, stream);
+        // Balanced tree split (ts_stream.cu launch_balanced, same scheme): one
+        // CTA walks a 32..256-row tile over ALL trees, so any batch up to one
+        // wave of tiles costs the whole ensemble's walk (config 3's 5000
+        // trees: 135 us from 1 to 4000 rows).  Unit weights, no ordinals; a
+        // somewhat larger share of rows may take k_combine's second walk
+        // than for complete trees (the alternative is that much slower).
+        const int sms = dev_attrs(device).sms;
+        const long long tiles = (args.n + ca.B - 1) / ca.B;
+        const int T = args.t1 - args.t0;
+        const char *ske = getenv("TS_SK");
+        bool sk = args.unit_w && !args.ord && seg.slow_rows <= 2e-2f &&
+                  balanced_split_pays(seg.depth, T, tiles, sms, false, 16384) &&
+                  (tiles > sms || 10 * tiles <= 7 * sms);  // a first wave filled > 0.7 measured no gain (4000 rows: 135 -> 142 us)
+        if (ske) sk = atoi(ske) != 0 && args.unit_w && !args.ord;
+        const long long W = tiles * ca.nchunks;
+        long long ctas = std::min<long long>(sms, W);
+        if (const char *ce = getenv("TS_SK_CTAS")) ctas = std::min<long long>(std::max(1, atoi(ce)), W);
+        cudaMemPool_t pool = scratch_pool(device);
+        unsigned char *scratch = nullptr;
+        size_t psum_bytes = 0;
+        int slices = 0;
+        if (sk && pool && (ctas > tiles || tiles % ctas != 0)) {
+            slices = (int)((ctas + tiles - 1) / tiles) + 1;
+            psum_bytes = (size_t)tiles * slices * ca.B * sizeof(double);
+            if (cudaMallocFromPoolAsync((void **)&scratch, 2 * psum_bytes, pool, stream) != cudaSuccess) {
+                (void)cudaGetLastError();
+                scratch = nullptr;  // whole tiles instead
+            }
+        }
+        if (!scratch) return launch_cstream(ca, device, stream);
+        ca.sk_ctas = (int)ctas;
+        ca.sk_slices = slices;
+        ca.part_sum = reinterpret_cast<double *>(scratch);
+        ca.part_key = reinterpret_cast<uint32_t *>(scratch + psum_bytes);
+        cudaError_t e = launch_cstream(ca, device, stream);
+        if (e == cudaSuccess) {
+            LeafWalk g{};
+            g.rank = 2;
+            g.x = args.x;
+            g.ld = args.ld;
+            g.F = args.F;
+            g.seg = args.blob;
+            g.tree_off16 = args.tree_off16 + args.t0;
+            int xs = 0;  // records hold fid * 4 B: B = 32 G, a power of two
+            while ((1 << xs) < 4 * ca.B) xs++;
+            g.xshift = xs;
+            e = launch_combine(ca.part_sum, ca.part_key, slices, ca.B, tiles, ca.nchunks, (int)ctas, T,
+                               args.accumulate, args.out, args.n, g, stream);
+        }
+        const cudaError_t f = cudaFreeAsync(scratch, stream);
+        return e != cudaSuccess ? e : f;
     }
     if (seg.layout == kSplit) {
         StreamArgs sa{};

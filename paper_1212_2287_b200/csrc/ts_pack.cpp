@@ -514,7 +514,7 @@ extern "C" int ts_pack_ex(const ts_model_desc *d, int device, int flags, ts_mode
                                       off[t]});
         m->segments.back().rank_space = space;
     }
-    // kSplit / kRank segments: how often a row's tree-order sum may round (see
+    // Streaming segments: how often a row's tree-order sum may round (see
     // Segment::slow_rows).  The running sums of a row stay below about
     // M = 4 sqrt(sum_t mean(leaf_t^2)) + sum_t |mean(leaf_t)|; an add is exact
     // while the leaf's LSB, 2^(e - 23), is no finer than 2^(m - 53) with M <
@@ -523,7 +523,7 @@ extern "C" int ts_pack_ex(const ts_model_desc *d, int device, int flags, ts_mode
     // exact -- 2e-4 for N(0,1) leaves at T = 1000, most rows for leaves
     // spread over many decades.
     for (Segment &sg : m->segments) {
-        if (sg.layout != kSplit && sg.layout != kRank) continue;
+        if (sg.layout != kSplit && sg.layout != kRank && sg.layout != kCStream) continue;
         double sum_ms = 0.0, sum_mean = 0.0;
         std::vector<double> mags;
         for (int t = sg.t0; t < sg.t1; t++) {

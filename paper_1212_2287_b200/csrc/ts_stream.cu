@@ -287,10 +287,24 @@ __global__ void __launch_bounds__(256) k_fold(const double *terms, long long T, 
 //  * kSplit (ts_stream_kernel.cuh walk_group): header / top records / deep
 //    arrays, fp32 thresholds against the row's fp32 values;
 //  * kRank (ts_rank_kernel.cuh rank_group): 4-byte records fid << 24 | rank
-//    against the row's u16 ranks in its rank tile.
-__device__ __forceinline__ float leaf_walk_global(const unsigned char *tree, const LeafWalk &g,
-                                                  long long row) {
+//    against the row's u16 ranks in its rank tile;
+//  * kCStream (ts_cstream_kernel.cuh): child-index records of an irregular
+//    tree, down to its leaf.
+__device__ __forceinline__ float leaf_walk_global(const LeafWalk &g, long long t, long long row) {
     uint32_t j = 0;  // 0-based heap index
+    if (g.rank == 2) {
+        // kCStream: {x offset << 14 | left child's record, theta}; a leaf's x
+        // offset is the sentinel row F (ts_cstream_kernel.cuh)
+        const uint2 *recs = reinterpret_cast<const uint2 *>(g.seg + 16ull * __ldg(g.tree_off16 + t));
+        const float *xrow = g.x + row * g.ld;
+        for (;;) {
+            const uint2 q = __ldg(recs + j);
+            const uint32_t fid = q.x >> (14 + g.xshift);
+            if (fid >= (uint32_t)g.F) return __uint_as_float(q.y);
+            j = (q.x & 0x3fffu) + (__ldg(xrow + fid) >= __uint_as_float(q.y) ? 1u : 0u);
+        }
+    }
+    const unsigned char *tree = g.seg + t * g.tree_bytes;
     if (g.rank) {
         const uint16_t *rr = g.R + (row / kRankB) * g.F * kRankB + rank_slot((uint32_t)(row % kRankB));
         const uint32_t *recs = reinterpret_cast<const uint32_t *>(tree);
@@ -393,7 +407,7 @@ __global__ void __launch_bounds__(kCombineThreads)
         auto walk_batch = [&](long long t0, double *dst) {
             const long long t = t0 + (threadIdx.x - 32);
             if (threadIdx.x >= 32 && t < T) {
-                const float lv = leaf_walk_global(g.seg + t * g.tree_bytes, g, srow);
+                const float lv = leaf_walk_global(g, t, srow);
                 dst[threadIdx.x - 32] = g.weight ? __dmul_rn(__ldg(g.weight + t), (double)lv) : (double)lv;
             }
         };
@@ -436,8 +450,8 @@ cudaError_t launch_combine(const double *part_sum, const uint32_t *part_key, int
 // else does (the rank walk) -- or a second / third wave filled to at most 0.6
 // (d >= 6).  The walk must be long enough to carry the second launch.
 bool balanced_split_pays(int D, long long T, long long tiles, int resident,
-                         bool has_small_batch_paths) {
-    if (T > 4096 || T * D < 6000) return false;
+                         bool has_small_batch_paths, long long max_trees) {
+    if (T > max_trees || T * D < 6000) return false;
     const double fill = (double)tiles / resident;
     const int waves_done = (int)fill;
     const double frac = fill - waves_done;

@@ -617,12 +617,12 @@ def test_build_accepts_reference_kinds():
         build(ens, "no_such_kind")
 
 
-def _rand_unbalanced(rng, max_depth, f, prune=0.35):
+def _rand_unbalanced(rng, max_depth, f, prune=0.35, leaf=None):
     from paper_1212_2287_b200 import Node, Tree
 
     def build_node(level):
         if level == max_depth or (level > 0 and rng.random() < prune):
-            return Node.leaf(rng.random())
+            return Node.leaf(rng.random() if leaf is None else leaf())
         return Node.internal(int(rng.integers(f)), rng.random(), build_node(level + 1),
                              build_node(level + 1))
     return Tree(build_node(0))
@@ -637,6 +637,39 @@ def _rand_complete(rng, depth, f, leaf_scale=1.0):
         return Node.internal(int(rng.integers(f)), rng.random(), build_node(level + 1),
                              build_node(level + 1))
     return Tree(build_node(0))
+
+
+@pytest.mark.parametrize("kind", ["narrow", "wide", "zeros"])
+@pytest.mark.parametrize("f,n,ctas", [(40, 1, None), (40, 77, "9"), (40, 1500, None), (700, 300, None),
+                                      (136, 5000, "50")])
+def test_irregular_balanced_split(kind, f, n, ctas, monkeypatch):
+    """Balanced tree split on the irregular-tree kernel (k_cstream<..., SK>):
+    runs of (tile, chunk) items per CTA, the accumulator warp's partial sums
+    combined when provably exact, rows walked again from the child-index
+    records otherwise; unit weights; bit-exact, also from a running sum."""
+    import torch
+    from paper_1212_2287_b200 import Ensemble
+    monkeypatch.setenv("TS_SK", "1")
+    if ctas:
+        monkeypatch.setenv("TS_SK_CTAS", ctas)
+    rng = np.random.default_rng(f + n + len(kind))
+    leaf = {"narrow": lambda: rng.standard_normal() * 0.05,
+            "wide": lambda: rng.standard_normal() * 10.0 ** rng.uniform(-30, 10),
+            "zeros": lambda: float(rng.choice([0.0, -0.0, 1e-45, -3e-42, 0.25, -1.5]))}[kind]
+    trees = [(_rand_unbalanced(rng, int(rng.integers(2, 13)), f, prune=0.3, leaf=leaf), 1.0)
+             for _ in range(260)]
+    ens = Ensemble(f, trees)
+    X = rng.random((n, f), dtype=np.float32)
+    X[rng.random((n, f)) < 0.3] = 0.0
+    s, o = oracle.COracle(ens.flat().arrays()).score(X, threads=4, with_ordinals=True)
+    ev = _ev(ens)
+    assert ev.model.info["compact_trees"] >= 150   # (a few random trees come out complete)
+    assert np.array_equal(ev.predict_batch(X).view(np.uint64), s.view(np.uint64))
+    assert np.array_equal(ev.leaf_indices(X), o.astype(np.int64))
+    monkeypatch.setenv("TS_FOLD_FAST", "0")   # every shared tile's rows on the second walk
+    assert np.array_equal(ev.score_device(torch.from_numpy(X).cuda()).cpu().numpy().view(np.uint64),
+                          s.view(np.uint64))
+    ev.close()
 
 
 def test_acceptance_cross_strategy_schedule():
