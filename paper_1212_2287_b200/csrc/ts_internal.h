@@ -104,6 +104,17 @@ struct DeviceTables {
     uint32_t *trace_base = nullptr;  // [T] first node of tree t
     // kRank: the rank spaces (RankSpace; a segment of kRank trees uses one)
     std::vector<RankSpace> rank_spaces;
+    // Balanced tree split, observed: {rows scored a second time by k_combine,
+    // rows of the tiles it combined} counted on the device (slow_dev); a CTA
+    // that saw such rows (and CTA 0) also posts the running totals into
+    // mapped pinned host memory (slow_seen; slow_seen_dev is its device
+    // address) -- plain stores, last writer wins, good enough for a heuristic
+    // (a stream-ordered copy after each call cost ~10 us of latency).  The pack-time estimate (Segment::slow_rows) knows the leaves
+    // but not how often the data reaches the tiny ones; once > 3 % of the
+    // combined rows needed the second walk the planner stops splitting this
+    // model (balanced_split_trusted).
+    unsigned int *slow_dev = nullptr;
+    unsigned int *slow_seen = nullptr, *slow_seen_dev = nullptr;
 };
 
 
@@ -312,6 +323,7 @@ struct StreamArgs {
     // again in the blob and adds the leaves in tree order.
     int sk_ctas, sk_slices;
     float slow_rows;  // Segment::slow_rows
+    const DeviceTables *tables;  // observed second-walk counters (may be null)
     uint32_t lb_bytes;  // warp-split kernel (k_stream_ws): two tpc x 32 fp32 leaf buffers
     int ws_ctas;        // warp-split kernel: CTAs per SM (2 or 3)
     int k;              // k_stream lockstep chains per thread (chains_for_depth / _fallback)
@@ -379,6 +391,7 @@ struct LeafWalk {
     const unsigned char *seg; // first tree of the segment (kCStream: the blob)
     const double *weight;     // nullptr: unit weights
     const uint32_t *tree_off16;  // kCStream: tree t of the segment at 16 * tree_off16[t]
+    unsigned int *slow_dev, *slow_seen_dev;  // DeviceTables::slow_dev / slow_seen_dev (may be null)
     int xshift;               // kCStream: record x offset = fid << xshift (4 B bytes per feature)
 };
 cudaError_t launch_combine(const double *part_sum, const uint32_t *part_key, int slices, int B,
@@ -386,7 +399,9 @@ cudaError_t launch_combine(const double *part_sum, const uint32_t *part_key, int
                            double *out, long long n, const LeafWalk &walk, cudaStream_t stream);
 // The planner's test for the balanced split (fill of the last wave of tiles).
 bool balanced_split_pays(int D, long long T, long long tiles, int resident, bool has_small_batch_paths,
-                         long long max_trees = 4096);
+                         long long max_trees = 16384);
+// false once the model's observed share of second-walk rows says the split does not pay
+bool balanced_split_trusted(const DeviceTables *t);
 bool rank_plan_ok(int F, int D, int device);
 cudaError_t launch_rank_segment(const Segment &seg, const ScoreArgs &args, int device,
                                 cudaStream_t stream);

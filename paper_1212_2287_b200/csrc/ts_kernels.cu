@@ -340,6 +340,7 @@ cudaError_t launch_segment(const Segment &seg, const ScoreArgs &args0, int devic
         const int T = args.t1 - args.t0;
         const char *ske = getenv("TS_SK");
         bool sk = args.unit_w && !args.ord && seg.slow_rows <= 2e-2f &&
+                  balanced_split_trusted(args.tables) &&
                   balanced_split_pays(seg.depth, T, tiles, sms, false, 16384) &&
                   (tiles > sms || 10 * tiles <= 7 * sms);  // a first wave filled > 0.7 measured no gain (4000 rows: 135 -> 142 us)
         if (ske) sk = atoi(ske) != 0 && args.unit_w && !args.ord;
@@ -375,6 +376,8 @@ cudaError_t launch_segment(const Segment &seg, const ScoreArgs &args0, int devic
             int xs = 0;  // records hold fid * 4 B: B = 32 G, a power of two
             while ((1 << xs) < 4 * ca.B) xs++;
             g.xshift = xs;
+            g.slow_dev = args.tables->slow_dev;
+            g.slow_seen_dev = args.tables->slow_seen_dev;
             e = launch_combine(ca.part_sum, ca.part_key, slices, ca.B, tiles, ca.nchunks, (int)ctas, T,
                                args.accumulate, args.out, args.n, g, stream);
         }
@@ -391,6 +394,7 @@ cudaError_t launch_segment(const Segment &seg, const ScoreArgs &args0, int devic
             sa.blob = args.blob;
             sa.seg_byte0 = seg.byte0;
             sa.slow_rows = seg.slow_rows;
+            sa.tables = args.tables;
             sa.weight = args.weight;
             sa.t0 = args.t0;
             sa.t1 = args.t1;

@@ -252,6 +252,8 @@ void free_tables(DeviceTables *t) {
     cudaFree(t->trace_base);
     cudaFree(t->chunk_info);
     cudaFree(t->slot_meta);
+    cudaFree(t->slow_dev);
+    cudaFreeHost(t->slow_seen);
     for (RankSpace &r : t->rank_spaces) {
         cudaFree(r.e);
         cudaFree(r.eoff);
@@ -596,6 +598,21 @@ extern "C" int ts_pack_ex(const ts_model_desc *d, int device, int flags, ts_mode
     if (!rc) rc = upload(&m->dev.weight, weight);
     if (!rc) rc = upload(&m->dev.chunk_info, chunk_info);
     if (!rc) rc = upload(&m->dev.slot_meta, slot_meta);
+    if (!rc) {  // second-walk counters (DeviceTables::slow_dev / slow_seen); optional
+        if (cudaMalloc((void **)&m->dev.slow_dev, 2 * sizeof(unsigned int)) != cudaSuccess ||
+            cudaMemset(m->dev.slow_dev, 0, 2 * sizeof(unsigned int)) != cudaSuccess ||
+            cudaHostAlloc((void **)&m->dev.slow_seen, 2 * sizeof(unsigned int), cudaHostAllocMapped) !=
+                cudaSuccess ||
+            cudaHostGetDevicePointer((void **)&m->dev.slow_seen_dev, m->dev.slow_seen, 0) != cudaSuccess) {
+            (void)cudaGetLastError();
+            cudaFree(m->dev.slow_dev);
+            cudaFreeHost(m->dev.slow_seen);
+            m->dev.slow_dev = nullptr;
+            m->dev.slow_seen = m->dev.slow_seen_dev = nullptr;
+        } else {
+            m->dev.slow_seen[0] = m->dev.slow_seen[1] = 0u;
+        }
+    }
     for (size_t sp = 0; !rc && sp < rank_hosts.size(); sp++) {
         // Eytzinger trees of the space's sorted lists (see RankSpace), and the
         // pre-pass's feature groups: consecutive features whose trees share

@@ -273,6 +273,7 @@ cudaError_t rank_chunk(const Segment &seg, const ScoreArgs &args, int device,
         const int nchunks = (T + a.tpc - 1) / a.tpc;
         const char *ske = getenv("TS_SK");
         bool sk = args.unit_w && !args.ord && seg.slow_rows <= 1e-3f &&
+                  balanced_split_trusted(args.tables) &&
                   balanced_split_pays(seg.depth, T, tiles, sms, false);
         if (ske) sk = atoi(ske) != 0 && args.unit_w && !args.ord;
         const long long W = tiles * nchunks;
@@ -306,6 +307,8 @@ cudaError_t rank_chunk(const Segment &seg, const ScoreArgs &args, int device,
                 g.R = R;
                 g.F = args.F;
                 g.seg = args.blob + seg.byte0;
+                g.slow_dev = dt.slow_dev;
+                g.slow_seen_dev = dt.slow_seen_dev;
                 e = launch_combine(a.part_sum, a.part_key, slices, kRankB, tiles, nchunks, (int)ctas,
                                    T, args.accumulate, args.out, args.n, g, stream);
             }

@@ -400,6 +400,15 @@ __global__ void __launch_bounds__(kCombineThreads)
     }
     __syncthreads();
     const int ns = n_slow;
+    if (threadIdx.x == 0 && g.slow_dev) {  // DeviceTables::slow_dev, slow_seen
+        const unsigned int rows = (unsigned int)min((long long)B, n - tile * B);
+        const unsigned int s1 = atomicAdd(g.slow_dev + 1, rows) + rows;
+        const unsigned int s0 = ns ? atomicAdd(g.slow_dev, (unsigned int)ns) + ns : 0u;
+        if (g.slow_seen_dev && (ns || blockIdx.x == 0)) {
+            if (ns) g.slow_seen_dev[0] = s0;
+            g.slow_seen_dev[1] = s1;
+        }
+    }
     for (int i = 0; i < ns; i++) {
         const long long srow = tile * B + slow_rows[i];
         double acc = 0.0;
@@ -438,6 +447,12 @@ cudaError_t launch_combine(const double *part_sum, const uint32_t *part_key, int
         ff && atoi(ff) == 0 ? 1 : 0);
     count_launch();
     return cudaGetLastError();
+}
+
+bool balanced_split_trusted(const DeviceTables *t) {
+    if (!t || !t->slow_seen) return true;
+    const unsigned int slow = t->slow_seen[0], rows = t->slow_seen[1];
+    return !(rows >= 2048u && (unsigned long long)slow * 100ull > 3ull * rows);
 }
 
 // Where the balanced split measured faster (profiles/r2_balanced_split.txt):
@@ -514,6 +529,8 @@ static cudaError_t launch_balanced(int D, const StreamArgs &a, int ctas, long lo
         g.ld = a.ld;
         g.seg = a.blob + a.seg_byte0;
         g.weight = a.unit_w ? nullptr : a.weight + a.t0;
+        g.slow_dev = a.tables ? a.tables->slow_dev : nullptr;
+        g.slow_seen_dev = a.tables ? a.tables->slow_seen_dev : nullptr;
         e = launch_combine(w.part_sum, w.part_key, slices, B, tiles, nchunks, ctas, T, a.accumulate,
                            a.out, a.n, g, stream);
     }
@@ -561,7 +578,7 @@ cudaError_t launch_stream(int D, const StreamArgs &a0, int device, cudaStream_t 
     // overrides the CTA count (tests, A/B).
     {
         const char *ske = getenv("TS_SK");
-        bool sk = a.unit_w && long_walk && a.slow_rows <= 1e-3f &&
+        bool sk = a.unit_w && long_walk && a.slow_rows <= 1e-3f && balanced_split_trusted(a.tables) &&
                   balanced_split_pays(D, T, tiles, resident, true) && !getenv("TS_SPLIT") &&
                   !getenv("TS_WS");
         if (ske) sk = atoi(ske) != 0;

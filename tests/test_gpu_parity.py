@@ -672,6 +672,38 @@ def test_irregular_balanced_split(kind, f, n, ctas, monkeypatch):
     ev.close()
 
 
+def test_balanced_split_learns_from_second_walks(monkeypatch):
+    """One tiny leaf that every row reaches: the packer's estimate (one leaf
+    in ~30,000) lets the planner split, every shared tile's rows then need
+    k_combine's second walk, and the model's observed counters
+    (DeviceTables::slow_seen) make the next calls walk whole tiles again --
+    bit-exact before and after."""
+    import torch
+    from paper_1212_2287_b200 import Ensemble, Node, Tree, _lib
+    monkeypatch.setenv("TS_FORCE_CSTREAM", "1")   # one irregular-kernel segment
+    rng = np.random.default_rng(404)
+    f = 40
+    leaf = lambda: rng.standard_normal() * 0.05  # noqa: E731
+    trees = [(_rand_unbalanced(rng, 9, f, prune=0.12, leaf=leaf), 1.0) for _ in range(720)]
+    hot = Tree(Node.internal(0, -1.0, Node.leaf(0.1),
+                             Node.internal(1, -1.0, Node.leaf(0.2), Node.leaf(1e-12))))
+    trees.insert(5, (hot, 1.0))
+    ens = Ensemble(f, trees)
+    n = 1500
+    X = rng.random((n, f), dtype=np.float32)
+    s = oracle.COracle(ens.flat().arrays()).score(X, threads=4)
+    ev = _ev(ens)
+    xd = torch.from_numpy(X).cuda()
+    launches = []
+    for _ in range(3):
+        before = _lib.launch_count()
+        got = ev.score_device(xd).cpu().numpy()   # (the copy back synchronises)
+        launches.append(_lib.launch_count() - before)
+        assert np.array_equal(got.view(np.uint64), s.view(np.uint64))
+    assert launches[0] == 2 and launches[-1] == 1, launches
+    ev.close()
+
+
 def test_acceptance_cross_strategy_schedule():
     """The reference's acceptance criterion 1 (ref tests/test_acceptance.py:
     83-125) on the GPU: 200 ensembles over f = 32/128/512 with its schedule
