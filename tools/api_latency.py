@@ -2,6 +2,7 @@
 and predict on numpy input, vs the device-only kernel time.
 
     python tools/api_latency.py [--depth 8] [--trees 1000]
+    python tools/api_latency.py --irregular [--trees 5000]    # config 3's ensemble (F = 700)
 """
 import argparse
 import os
@@ -20,12 +21,17 @@ def main():
     ap.add_argument("--depth", type=int, default=8)
     ap.add_argument("--trees", type=int, default=1000)
     ap.add_argument("--reps", type=int, default=200)
+    ap.add_argument("--irregular", action="store_true")
     a = ap.parse_args()
     rng = np.random.default_rng(1)
     d, T, F = a.depth, a.trees, 136
-    n_int = (1 << d) - 1
-    flat = synth.complete_flat(F, d, rng.integers(0, F, (T, n_int)), rng.random((T, n_int)),
-                               rng.standard_normal((T, 1 << d)))
+    if a.irregular:
+        w = synth.config3(n=1, trees=T)
+        flat, F, d = w.flat, w.f, "irr"
+    else:
+        n_int = (1 << d) - 1
+        flat = synth.complete_flat(F, d, rng.integers(0, F, (T, n_int)), rng.random((T, n_int)),
+                                   rng.standard_normal((T, 1 << d)))
     ev = build_gpu(flat)
     for n in (1, 10, 100, 1000, 10000):
         x = rng.random((n, F), dtype=np.float32)
